@@ -1,0 +1,658 @@
+// ys_assemble.cu — local evaluation, deterministic assembly and the block
+// Jacobi build.
+//
+// Reference: Engine::assemble (engine.cpp:47-60) -> assemble_group
+// (assembly.cpp:323-374) -> assemble_local (284-321) -> serial scatter
+// (346-372); DiagAccumulator (158-180); BlockJacobiPreconditioner::build
+// (solver.cpp:93-122); Engine::total_energy (engine.cpp:64-68).
+//
+// Flow per Newton iteration:
+//   1. one eval kernel per energy writes every instance's raw-slot gradient
+//      and its oriented ublock-pair Hessian blocks into the group buffers
+//      (contiguous per instance: coalesced stores);
+//   2. k_gather_h sums the k-th sorted run of block contributions into
+//      unique block k in (energy, instance) order — bit-identical to the
+//      reference's serial `+=` for identical local blocks;
+//   3. k_block_rows (one thread per target instance) gathers the gradient
+//      (static runs then dynamic runs, the reference's order), forms the
+//      DiagAccumulator block (static H block + dynamic contributions one by
+//      one) and inverts it for the preconditioner.
+#include <algorithm>
+#include <cstdio>
+
+#include "ys_device.cuh"
+
+namespace ys {
+
+namespace {
+constexpr int kTB = 256;
+inline unsigned grid_for(int64_t n, int tb = kTB) { return unsigned(std::max<int64_t>(1, ceil_div(n, tb))); }
+}  // namespace
+
+// error flag bits (NumericalError sources in eval.cpp)
+constexpr int kErrLog = 1;  // "log of non-positive value" (eval.cpp:296-301)
+constexpr int kErrDiv = 2;  // "division by zero" (eval.cpp:226-237)
+
+EnergyDev energy_dev(Context& c, Energy& e) {
+  EnergyDev E{};
+  E.kind = e.kind;
+  E.kappa = e.kappa;
+  E.width = e.width;
+  E.mode = e.mode;
+  E.n = e.n;
+  E.conn = e.conn.p;
+  E.cdata = e.cdata.p;
+  E.anchor = e.anchor.p;
+  E.startP = e.target >= 0 ? int32_t(c.targets[e.target].start) : 0;
+  if (e.domain >= 0) {
+    const Domain& d = c.domains[e.domain];
+    E.dom.kind = d.kind;
+    E.dom.n = d.n;
+    E.dom.startA = d.ta >= 0 ? int32_t(c.targets[d.ta].start) : 0;
+    E.dom.startB = d.tb >= 0 ? int32_t(c.targets[d.tb].start) : 0;
+    E.dom.v2b = d.v2b.p;
+    E.dom.rest = d.rest.p;
+    E.dom.fixed = d.rest.p;
+  }
+  if (e.pairset >= 0) {
+    const PairSet& ps = c.pairsets[e.pairset];
+    const Union& u = c.unions[ps.uni];
+    E.uni.nchild = int32_t(u.children.size());
+    E.uni.kappa_u = u.kappa_u;
+    E.uni.width = u.width;
+    E.uni.child = u.d_child.p;
+    E.uni.offsets = u.d_offsets.p;
+    E.pairs = ps.pairs.p;
+  }
+  for (int k = 0; k < 6; ++k) E.prm[k] = e.prm[k];
+  E.slots = e.slots.p;
+  E.m = e.m.p;
+  E.hoff = e.uniform ? nullptr : e.hoff.p;
+  E.goff = e.uniform ? nullptr : e.goff.p;
+  E.doff = e.uniform ? nullptr : e.doff.p;
+  E.soff = e.uniform ? nullptr : e.soff.p;
+  E.hstride = e.hstride;
+  E.gstride = e.gstride;
+  E.dstride = e.dstride;
+  E.sstride = e.sstride;
+  E.hbase = e.hbase;
+  E.gbase = e.gbase;
+  E.dbase = e.dbase;
+  E.sbase = e.sbase;
+  return E;
+}
+
+// ---------------------------------------------------------------------------
+// Evaluation kernels
+
+struct VertexBlockWriter {
+  double* h;
+  uint32_t swap;  // bit p: store pair p transposed (gstart(a) > gstart(b))
+  __device__ __forceinline__ void operator()(int pair, int k, int kk, double v) const {
+    h[pair * 9 + (((swap >> pair) & 1u) ? kk * 3 + k : k * 3 + kk)] = v;
+  }
+};
+
+__device__ __forceinline__ uint32_t vertex_pair_swaps(const int32_t gs[4]) {
+  uint32_t sw = 0;
+  int pair = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = a; b < 4; ++b, ++pair)
+      if (gs[a] > gs[b]) sw |= 1u << pair;
+  return sw;
+}
+
+__device__ __forceinline__ void load_stencil(const EnergyDev& E, const double* __restrict__ X, int64_t i,
+                                             double x[12], int32_t gs[4]) {
+  const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
+  const int vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    gs[l] = E.startP + 3 * vv[l];
+    const double* q = X + gs[l];
+    x[3 * l + 0] = q[0];
+    x[3 * l + 1] = q[1];
+    x[3 * l + 2] = q[2];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_eval_snh(EnergyDev E, const double* __restrict__ X, int project,
+                                                  int want_h, double* __restrict__ hc, double* __restrict__ gc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double x[12];
+  int32_t gs[4];
+  load_stencil(E, X, i, x, gs);
+  double binv[9];
+  const double* cd = E.cdata + 10 * i;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) binv[k] = cd[k];
+  const double vol = cd[9];
+  const SnhParams P{E.prm[0], E.prm[1], E.prm[2], E.prm[3]};
+  double g[12];
+  VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
+  snh_local(x, binv, vol, P, want_h != 0, project != 0, E.mode == YS_PROJECT_REDUCED, g, wr);
+  double* go = gc + inst_goff(E, i);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) go[k] = g[k];
+}
+
+__global__ void __launch_bounds__(128) k_eval_bending(EnergyDev E, const double* __restrict__ X, int project,
+                                                      int want_h, double* __restrict__ hc,
+                                                      double* __restrict__ gc, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double x[12];
+  int32_t gs[4];
+  load_stencil(E, X, i, x, gs);
+  double g[12];
+  VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
+  const int st = bending_local(x, E.cdata[i], want_h != 0, project != 0, g, wr);
+  if (st) atomicOr(err, kErrDiv);
+  double* go = gc + inst_goff(E, i);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) go[k] = g[k];
+}
+
+__global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* __restrict__ X, int project,
+                                                    int want_h, double* __restrict__ hc, double* __restrict__ gc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double A[9];
+  const double* q = X + E.startP + 9 * i;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) A[k] = q[k];
+  double g[9];
+  ortho_local(A, E.prm[0], want_h != 0, project != 0, g, hc + inst_hoff(E, i));
+  double* go = gc + inst_goff(E, i);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) go[k] = g[k];
+}
+
+// Inertia and pair energies: one 3-vector delta, linear in the compressed DoFs.
+__global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int project, int want_h,
+                             double* __restrict__ hc, double* __restrict__ gc, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  PSlot s[kMaxKappa];
+  energy_slots(E, i, s);
+  double dl[3], gd[3], P[9];
+  if (E.kind == K_INERTIA) {
+    double p[3];
+    point_position(E.dom, i, X, p);
+    const double* xt = E.anchor + 3 * i;
+    const double m = E.cdata[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dl[k] = p[k] - xt[k];
+      gd[k] = m * dl[k];
+    }
+    proj_rank1_3(m, 0.0, dl, 1.0, project != 0, P);
+  } else {
+    double p0[3], p1[3];
+    int64_t l0, l1;
+    const int c0 = union_decode(E.uni, E.pairs[2 * i], &l0);
+    const int c1 = union_decode(E.uni, E.pairs[2 * i + 1], &l1);
+    point_position(E.uni.child[c0], l0, X, p0);
+    point_position(E.uni.child[c1], l1, X, p1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dl[k] = p1[k] - p0[k];
+    const double d = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+    const PairParams PP{E.prm[0], E.prm[1], E.prm[2], E.kind == K_REPULSIVE};
+    double b, b1, b2;
+    const int st = pair_b(d, PP, &b, &b1, &b2);
+    if (st) atomicOr(err, st == 1 ? kErrLog : kErrDiv);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gd[k] = 2.0 * b1 * dl[k];
+    proj_rank1_3(2.0 * b1, 4.0 * b2, dl, d, project != 0, P);
+  }
+  write_point_gradient(s, E.kappa, gd, gc + inst_goff(E, i));
+  if (want_h) {
+    UBlocks u;
+    make_ublocks(s, E.kappa, u);
+    write_point_blocks(u, P, hc + inst_hoff(E, i));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Energy-only kernels (line search): per-instance energy into out[i].
+
+__global__ void k_energy(EnergyDev E, const double* __restrict__ X, double* __restrict__ out, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double e = 0.0;
+  switch (E.kind) {
+    case K_SNH: {
+      double x[12];
+      int32_t gs[4];
+      load_stencil(E, X, i, x, gs);
+      const double* cd = E.cdata + 10 * i;
+      double binv[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) binv[k] = cd[k];
+      const SnhParams P{E.prm[0], E.prm[1], E.prm[2], E.prm[3]};
+      if (!snh_energy(x, binv, cd[9], P, &e)) atomicOr(err, kErrLog);
+      break;
+    }
+    case K_BENDING: {
+      double x[12];
+      int32_t gs[4];
+      load_stencil(E, X, i, x, gs);
+      if (bending_energy(x, E.cdata[i], &e)) atomicOr(err, kErrDiv);
+      break;
+    }
+    case K_ORTHO: {
+      double A[9];
+      const double* q = X + E.startP + 9 * i;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) A[k] = q[k];
+      e = ortho_energy(A, E.prm[0]);
+      break;
+    }
+    case K_INERTIA: {
+      double p[3];
+      point_position(E.dom, i, X, p);
+      const double* xt = E.anchor + 3 * i;
+      double d2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d2 += (p[k] - xt[k]) * (p[k] - xt[k]);
+      e = 0.5 * E.cdata[i] * d2;
+      break;
+    }
+    default: {
+      double p0[3], p1[3];
+      int64_t l0, l1;
+      const int c0 = union_decode(E.uni, E.pairs[2 * i], &l0);
+      const int c1 = union_decode(E.uni, E.pairs[2 * i + 1], &l1);
+      point_position(E.uni.child[c0], l0, X, p0);
+      point_position(E.uni.child[c1], l1, X, p1);
+      double d = 0.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) d += (p1[k] - p0[k]) * (p1[k] - p0[k]);
+      const PairParams PP{E.prm[0], E.prm[1], E.prm[2], E.kind == K_REPULSIVE};
+      double b1, b2;
+      const int st = pair_b(d, PP, &e, &b1, &b2);
+      if (st) atomicOr(err, st == 1 ? kErrLog : kErrDiv);
+      break;
+    }
+  }
+  out[i] = e;
+}
+
+// Deterministic sum: fixed grid of partials, then one block sums them in order.
+__global__ void k_sum_partials(const double* __restrict__ v, int64_t n, double* __restrict__ part) {
+  __shared__ double sm[kTB];
+  double acc = 0.0;
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+    acc += v[j];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w /= 2) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+// ---------------------------------------------------------------------------
+// Assembly gather: unique block u = sum of its sorted contribution run.
+__global__ void k_gather_h(const int64_t* __restrict__ seg, const uint32_t* __restrict__ perm,
+                           const double* __restrict__ hc, int64_t u0, int64_t cnt, int rc,
+                           const int64_t* __restrict__ voff, double* __restrict__ values) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= cnt * rc) return;
+  const int64_t u = u0 + t / rc;
+  const int e = int(t % rc);
+  const int64_t j0 = seg[u], j1 = seg[u + 1];
+  double acc = 0.0;
+  for (int64_t j = j0; j < j1; ++j) acc += hc[perm[j] + e];
+  values[voff[u] + e] = acc;
+}
+
+struct GroupView {
+  const int32_t* gseg;
+  const uint32_t* gperm;
+  const double* gcontrib;
+  const int32_t* diag_uid;
+  const int64_t* seg;
+  const uint32_t* perm;
+  const double* hcontrib;
+  const double* values;
+  const int64_t* voff;
+};
+
+// Inverse by Gaussian elimination with partial pivoting (PartialPivLU, the
+// algorithm behind Eigen's dynamic-size inverse(), solver.cpp:107).
+template <int N>
+__device__ __forceinline__ void lu_inverse(const double* B, double* inv) {
+  double a[N * N];
+  int piv[N];
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) a[k] = B[k];
+#pragma unroll
+  for (int k = 0; k < N; ++k) piv[k] = k;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    int p = k;
+    double best = fabs(a[k * N + k]);
+#pragma unroll
+    for (int r = k + 1; r < N; ++r)
+      if (fabs(a[r * N + k]) > best) {
+        best = fabs(a[r * N + k]);
+        p = r;
+      }
+    if (p != k) {
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        const double t = a[k * N + c];
+        a[k * N + c] = a[p * N + c];
+        a[p * N + c] = t;
+      }
+      const int t = piv[k];
+      piv[k] = piv[p];
+      piv[p] = t;
+    }
+    const double d = a[k * N + k];
+#pragma unroll
+    for (int r = k + 1; r < N; ++r) {
+      const double f = a[r * N + k] / d;
+      a[r * N + k] = f;
+#pragma unroll
+      for (int c = k + 1; c < N; ++c) a[r * N + c] -= f * a[k * N + c];
+    }
+  }
+  // solve L U X = P I column by column
+#pragma unroll
+  for (int col = 0; col < N; ++col) {
+    double y[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double v = (piv[r] == col) ? 1.0 : 0.0;
+#pragma unroll
+      for (int c = 0; c < r; ++c) v -= a[r * N + c] * y[c];
+      y[r] = v;
+    }
+#pragma unroll
+    for (int r = N - 1; r >= 0; --r) {
+      double v = y[r];
+#pragma unroll
+      for (int c = r + 1; c < N; ++c) v -= a[r * N + c] * y[c];
+      y[r] = v / a[r * N + r];
+    }
+#pragma unroll
+    for (int r = 0; r < N; ++r) inv[r * N + col] = y[r];
+  }
+}
+
+// BlockJacobiPreconditioner::build for one block (solver.cpp:98-120).
+// Returns 0 ok, 1 identity fallback, 2 regularized, 3 singular.
+template <int N>
+__device__ __forceinline__ int jacobi_block_inverse(const double* B, double* inv) {
+  bool zero = true;
+  double nb = 0.0, tr = 0.0;
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) {
+    zero = zero && (fabs(B[k]) <= 0.0);
+    nb += B[k] * B[k];
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) tr += B[k * N + k];
+  if (zero) {
+#pragma unroll
+    for (int k = 0; k < N * N; ++k) inv[k] = (k % (N + 1) == 0) ? 1.0 : 0.0;
+    return 1;
+  }
+  auto residual = [&](const double* M, const double* I) {
+    double r = 0.0;
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) acc += M[i * N + k] * I[k * N + j];
+        acc -= (i == j) ? 1.0 : 0.0;
+        r += acc * acc;
+        finite = finite && isfinite(I[i * N + j]);
+      }
+    return finite ? sqrt(r) : INFINITY;
+  };
+  lu_inverse<N>(B, inv);
+  if (residual(B, inv) <= 1e-6 * (1.0 + sqrt(nb))) return 0;
+  double eps = 1e-12 * tr / N;
+  if (!(eps > 0.0)) eps = 1e-12;
+  double reg[N * N];
+  double nr = 0.0;
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) {
+    reg[k] = B[k] + ((k % (N + 1) == 0) ? eps : 0.0);
+    nr += reg[k] * reg[k];
+  }
+  lu_inverse<N>(reg, inv);
+  if (!(residual(reg, inv) <= 1e-3 * (1.0 + sqrt(nr)))) return 3;
+  return 2;
+}
+
+template <int N>
+__device__ __forceinline__ void block_row_work(int64_t b, const BlocksDev& B, const GroupView& S0,
+                                               const GroupView& S1, double* G, double* diag, double* minv,
+                                               int32_t* bflag, int want_h) {
+  const int32_t st = B.start[b];
+  double acc[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int gi = 0; gi < 2; ++gi) {
+    const GroupView& S = gi == 0 ? S0 : S1;
+    if (!S.gseg) continue;
+    const int32_t j0 = S.gseg[b], j1 = S.gseg[b + 1];
+    for (int32_t j = j0; j < j1; ++j) {
+      const double* src = S.gcontrib + (S.gperm[j] & 0x0FFFFFFFu);
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc[k] += src[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) G[st + k] = acc[k];
+  if (!want_h) return;
+  double blk[N * N];
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) blk[k] = 0.0;
+  if (S0.diag_uid) {
+    const int32_t u = S0.diag_uid[b];
+    if (u >= 0) {
+      const double* v = S0.values + S0.voff[u];
+#pragma unroll
+      for (int k = 0; k < N * N; ++k) blk[k] = 0.0 + v[k];
+    }
+  }
+  if (S1.diag_uid) {
+    const int32_t u = S1.diag_uid[b];
+    if (u >= 0) {
+      const int64_t j0 = S1.seg[u], j1 = S1.seg[u + 1];
+      for (int64_t j = j0; j < j1; ++j) {
+        const double* src = S1.hcontrib + S1.perm[j];
+#pragma unroll
+        for (int k = 0; k < N * N; ++k) blk[k] += src[k];
+      }
+    }
+  }
+  double* dd = diag + B.voff[b];
+#pragma unroll
+  for (int k = 0; k < N * N; ++k) dd[k] = blk[k];
+  bflag[b] = jacobi_block_inverse<N>(blk, minv + B.voff[b]);
+}
+
+// One launch per target (uniform block size N within a target).
+template <int N>
+__global__ void k_block_rows(BlocksDev B, int64_t b0, int64_t nb, GroupView S0, GroupView S1, double* G,
+                             double* diag, double* minv, int32_t* bflag, int want_h) {
+  const int64_t b = b0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= b0 + nb) return;
+  block_row_work<N>(b, B, S0, S1, G, diag, minv, bflag, want_h);
+}
+
+// ---------------------------------------------------------------------------
+// Host orchestration
+
+static void check_err(Context& c) {
+  int h = 0;
+  YS_CUDA(cudaMemcpyAsync(&h, c.errflag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  YS_CUDA(cudaStreamSynchronize(c.stream));
+  if (h) {
+    c.errflag.zero(c.stream);
+    if (h & kErrLog) fail(YS_ERR_NUMERICAL, "log of non-positive value");
+    fail(YS_ERR_NUMERICAL, "division by zero");
+  }
+}
+
+static GroupView group_view(Structure& st, bool present) {
+  GroupView v{};
+  if (!present) return v;
+  v.gseg = st.gseg.p;
+  v.gperm = st.gperm.p;
+  v.gcontrib = st.gcontrib.p;
+  v.diag_uid = st.diag_uid.p;
+  v.seg = st.seg.p;
+  v.perm = st.perm.p;
+  v.hcontrib = st.hcontrib.p;
+  v.values = st.values.p;
+  v.voff = st.voff.p;
+  return v;
+}
+
+void ctx_block_rows(Context& c, bool want_h);
+
+static void record(Context& c, int idx) {
+  if (c.profiling) YS_CUDA(cudaEventRecord(c.ev[idx], c.stream));
+}
+
+void ctx_assemble(Context& c, bool project, bool with_hessian) {
+  if (c.seen_epoch != c.epoch)
+    fail(YS_ERR_VALIDATION, "dynamic structures are stale after resize_dynamic; call refresh_dynamic()");
+  cudaStream_t s = c.stream;
+  record(c, 1);
+  for (size_t id = 0; id < c.energies.size(); ++id) {
+    Energy& e = c.energies[id];
+    if (e.n == 0 || e.kappa == 0) continue;
+    Structure& st = c.S[e.dynamic ? 1 : 0];
+    EnergyDev E = energy_dev(c, e);
+    const int proj = project ? 1 : 0, wh = with_hessian ? 1 : 0;
+    switch (e.kind) {
+      case K_SNH:
+        k_eval_snh<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
+        break;
+      case K_BENDING:
+        k_eval_bending<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                          c.errflag.p);
+        break;
+      case K_ORTHO:
+        k_eval_ortho<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
+        break;
+      default:
+        k_eval_point<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                        c.errflag.p);
+    }
+    YS_LAUNCH_CHECK();
+    ++c.launches;
+  }
+  record(c, 2);
+  if (with_hessian) {
+    for (int w = 0; w < 2; ++w) {
+      Structure& st = c.S[w];
+      for (auto& g : st.groups) {
+        const int rc = int(g[0] * g[1]);
+        const int64_t cnt = g[3];
+        if (cnt == 0) continue;
+        k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc,
+                                                      st.voff.p, st.values.p);
+        YS_LAUNCH_CHECK();
+        ++c.launches;
+      }
+    }
+  }
+  record(c, 3);
+  ctx_block_rows(c, with_hessian);
+  record(c, 4);
+  check_err(c);
+  c.assembled = true;
+  c.assembled_h = with_hessian;
+}
+
+void ctx_block_rows(Context& c, bool want_h) {
+  const BlocksDev B = blocks_view(c);
+  const GroupView S0 = group_view(c.S[0], true), S1 = group_view(c.S[1], true);
+  const int wh = want_h ? 1 : 0;
+  for (const Target& t : c.targets) {
+    if (t.n == 0) continue;
+    const unsigned g = grid_for(t.n, 128);
+    switch (t.rc) {
+      case 1: k_block_rows<1><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 2: k_block_rows<2><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 3: k_block_rows<3><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 4: k_block_rows<4><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 6: k_block_rows<6><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 9: k_block_rows<9><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      case 12: k_block_rows<12><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
+      default: fail(YS_ERR_INTERNAL, "unsupported target block size");
+    }
+    YS_LAUNCH_CHECK();
+    ++c.launches;
+  }
+}
+
+// Flags of the last preconditioner build -> regularized count / singular error.
+void ctx_build_preconditioner(Context& c) {
+  std::vector<int32_t> fl = c.bflag.to_host(c.stream);
+  std::vector<int32_t> st, rc;
+  int32_t reg = 0;
+  for (int64_t b = 0; b < c.NB; ++b) {
+    if (fl[b] == 1 || fl[b] == 2) ++reg;
+    if (fl[b] == 3 || fl[b] == 4) {
+      if (st.empty()) {
+        st = c.bstart.to_host(c.stream);
+        rc = c.brc.to_host(c.stream);
+      }
+      fail(YS_ERR_NUMERICAL, "diagonal block at DoF range [" + std::to_string(st[b]) + ", " +
+                                 std::to_string(st[b] + rc[b]) + ") is singular");
+    }
+  }
+  c.regularized = reg;
+}
+
+double ctx_total_energy(Context& c, double* per_energy) {
+  cudaStream_t s = c.stream;
+  const int nparts = 256;
+  c.partials.resize(std::max<size_t>(c.partials.n, size_t(nparts) * (c.energies.size() + 1)));
+  std::vector<double> parts(size_t(nparts) * c.energies.size(), 0.0);
+  for (size_t id = 0; id < c.energies.size(); ++id) {
+    Energy& e = c.energies[id];
+    const int64_t n = e.pairset >= 0 ? c.pairsets[e.pairset].n : e.n;
+    if (n == 0) continue;
+    c.scratch.resize(std::max<size_t>(c.scratch.n, size_t(n)));
+    EnergyDev E = energy_dev(c, e);
+    E.n = n;  // Evaluator::total reads the current instance count (eval.cpp:394-401)
+    k_energy<<<grid_for(n, 128), 128, 0, s>>>(E, c.X.p, c.scratch.p, c.errflag.p);
+    YS_LAUNCH_CHECK();
+    k_sum_partials<<<nparts, kTB, 0, s>>>(c.scratch.p, n, c.partials.p + id * nparts);
+    YS_LAUNCH_CHECK();
+  }
+  if (!c.energies.empty())
+    YS_CUDA(cudaMemcpyAsync(parts.data(), c.partials.p, parts.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  check_err(c);
+  double sum = 0.0;
+  for (size_t id = 0; id < c.energies.size(); ++id) {
+    const int64_t n = c.energies[id].pairset >= 0 ? c.pairsets[c.energies[id].pairset].n : c.energies[id].n;
+    double t = 0.0;
+    if (n > 0)
+      for (int k = 0; k < nparts; ++k) t += parts[id * nparts + k];
+    if (per_energy) per_energy[id] = t;
+    sum += t;
+  }
+  return sum;
+}
+
+}  // namespace ys

@@ -1,0 +1,232 @@
+// ys_context.cuh — host-side state of one engine context.
+//
+// Mirrors what relsim::Engine owns (engine.hpp:66-79): the gradient layout,
+// the compiled static and dynamic energy groups, their BlockSparseHessian
+// structures, the gradient and the diagonal accumulator — all device
+// resident — plus the scene pieces the energies read (targets, point
+// domains, unions, pair primitives).
+#pragma once
+
+#include <array>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "ys_common.cuh"
+
+namespace ys {
+
+enum Kind : int32_t {
+  K_SNH = 0,       // add_stable_neo_hookean (energies.cpp:49-118)
+  K_BENDING = 1,   // add_bending (energies.cpp:129-155)
+  K_INERTIA = 2,   // add_inertia (energies.cpp:168-174)
+  K_ORTHO = 3,     // add_affine_orthogonality (energies.cpp:120-127)
+  K_PP = 4,        // add_point_point_barrier (energies.cpp:30-47)
+  K_REPULSIVE = 5  // add_repulsive_energy (energies.cpp:20-28)
+};
+
+const char* kind_name(int k);
+
+struct Target {
+  int64_t n = 0;
+  int32_t rc = 0;
+  int64_t start = 0;   // GradientLayout::boundaries[t]
+  int64_t block0 = 0;  // first target-instance block
+};
+
+struct Domain {
+  int32_t kind = 0;
+  int64_t n = 0;
+  int32_t ta = -1, tb = -1;
+  std::vector<int64_t> h_v2b;
+  std::vector<double> h_rest;  // affine rest / fixed positions
+  DevBuf<int32_t> v2b;
+  DevBuf<double> rest;
+  int kappa() const { return kind == YS_POINTS_FREE ? 1 : kind == YS_POINTS_AFFINE ? 2 : 0; }
+  int width() const { return kind == YS_POINTS_FREE ? 3 : kind == YS_POINTS_AFFINE ? 12 : 0; }
+};
+
+struct Union {
+  std::vector<int32_t> children;
+  int32_t kappa_u = 0, width = 0;
+  DevBuf<DomainDev> d_child;
+  DevBuf<int64_t> d_offsets;
+  std::vector<int64_t> offsets() const;
+};
+
+struct PairSet {
+  int32_t uni = -1;
+  bool dynamic = false;
+  int64_t n = 0;
+  std::vector<int64_t> h_pairs;
+  DevBuf<int32_t> pairs;  // 2n union-global indices
+};
+
+// A compiled energy term group (CompiledEnergy, assembly.hpp:75-103).
+struct Energy {
+  int32_t kind = 0;
+  std::string name;
+  bool dynamic = false;
+  int32_t mode = YS_PROJECT_FULL;
+  int64_t n = 0;  // instances
+  int32_t kappa = 0, width = 0;
+  double prm[6] = {0, 0, 0, 0, 0, 0};
+  int32_t target = -1, domain = -1, pairset = -1;
+  DevBuf<int32_t> conn;    // SNH/bending: 4 vertex ids per instance
+  DevBuf<double> cdata;    // SNH: Binv(9)+vol; bending: l0; inertia: mass
+  DevBuf<double> anchor;   // inertia: x_tilde (n x 3)
+  std::vector<double> h_mass;
+
+  // --- structure, rebuilt with the group
+  DevBuf<DSlot> slots;     // n x kappa
+  DevBuf<int32_t> m;       // compressed size per instance
+  DevBuf<uint32_t> hoff, goff, doff, soff;  // per-instance exclusive offsets
+  uint32_t hstride = 0, gstride = 0, dstride = 0, sstride = 0;  // uniform strides
+  bool uniform = true;
+  int64_t hbase = 0, gbase = 0, dbase = 0, sbase = 0;  // bases inside the group buffers
+  int64_t hsize = 0, gsize = 0, ndest = 0, nslot = 0;
+  std::set<int> compressed_sizes;
+  bool built = false;
+};
+
+// BlockSparseHessian (assembly.hpp:19-60) of one group plus its assembly and
+// SpMV plans.
+struct Structure {
+  std::vector<std::array<int64_t, 5>> groups;  // rows, cols, coord_start, count, value_start
+  int64_t n_blocks = 0, n_values = 0;
+  bool all33 = true;
+  DevBuf<int32_t> row, col;     // per unique block (scalar coordinates)
+  DevBuf<int8_t> br, bc;        // block shape per unique block
+  DevBuf<int64_t> voff;         // value offset per unique block
+  DevBuf<double> values;
+  // H assembly plan: contributions sorted by key; segment k = block k.
+  int64_t n_contrib = 0;
+  DevBuf<int64_t> seg;          // n_blocks + 1
+  DevBuf<uint32_t> perm;        // double offset of each sorted contribution
+  DevBuf<double> hcontrib;
+  // gradient plan: slot contributions sorted by gstart; segment per block row.
+  int64_t n_gcontrib = 0;
+  DevBuf<int32_t> gseg;         // NB + 1
+  DevBuf<uint32_t> gperm;
+  DevBuf<int32_t> glen;         // length of each sorted slot contribution
+  DevBuf<double> gcontrib;
+  DevBuf<int32_t> diag_uid;     // NB: unique block index of the (b,b) block, -1 if absent
+  // SpMV plan: full (both triangle) row lists over block rows.
+  DevBuf<int32_t> sp_rowptr;    // NB + 1
+  DevBuf<int32_t> sp_ent;       // uid | (transposed << 31)
+  int32_t max_row_len = 0;
+  uint64_t checksum = 0;
+  bool checksum_valid = false;
+};
+
+struct PcgState {
+  double gnorm, rz, php, alpha, beta, rel, tol, pad0;
+  long long it, max_iter, hist_cap;
+  int status;  // 0 running, 1 converged, 2 stagnated (pHp == 0), 3 curvature error, 4 residual error, 5 max_iter
+  int fail_it;
+  unsigned int counter1, counter2;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int err_cls = 0;
+  std::string version;
+
+  std::vector<Target> targets;
+  int64_t s = 0;
+  bool finalized = false;
+  std::vector<Domain> domains;
+  std::vector<Union> unions;
+  std::vector<PairSet> pairsets;
+  std::vector<Energy> energies;
+  uint64_t epoch = 0, seen_epoch = 0;
+
+  // DoF state
+  DevBuf<double> X, X0, G, DX;
+  std::vector<std::vector<double>> h_target_init;
+
+  // block rows (target instances)
+  int64_t NB = 0, diag_vals = 0;
+  bool uniform3 = true;
+  DevBuf<int32_t> bstart, brc, dof2block;
+  DevBuf<int64_t> bvoff;
+  DevBuf<double> diag, minv;
+  DevBuf<int32_t> bflag;  // preconditioner: 0 ok, 1 identity fallback, 2 regularized, 3 singular
+  int32_t regularized = 0;
+
+  Structure S[2];  // 0 static, 1 dynamic
+  bool assembled = false, assembled_h = false;
+
+  // PCG
+  DevBuf<double> r, z, p, hp;
+  DevBuf<PcgState> pcg;
+  DevBuf<double> partials;
+  DevBuf<double> hist;
+  int64_t hist_count = 0;
+  int pcg_blocks = 0;
+  cudaGraphExec_t pcg_exec = nullptr;
+  cudaGraph_t pcg_graph = nullptr;
+  bool pcg_cond = false;
+  std::vector<uint64_t> pcg_key;
+  DevBuf<double> scratch;
+  DevBuf<int> errflag;
+
+  // structure-build scratch (reused across dynamic rebuilds)
+  DevBuf<unsigned char> cubtmp;
+  DevBuf<uint64_t> k_in, k_out, ukey;
+  DevBuf<uint32_t> p_in, gk_in, gk_out, gp_in;
+  DevBuf<int32_t> flags, incl, ghead, heads;
+  DevBuf<unsigned char> grpbuf;
+
+  // profiling
+  bool profiling = false;
+  double stage_ms[8] = {0};
+  int64_t launches = 0;
+  cudaEvent_t ev[10] = {};
+
+  // free-standing BSR systems (ys_bsr_*)
+  struct Bsr {
+    int64_t s = 0;
+    Structure st;
+    int64_t nb = 0;
+    std::vector<int64_t> h_rows, h_cols;
+  };
+  std::vector<Bsr> bsrs;
+};
+
+// --- host entry points implemented across the .cu files --------------------
+void ctx_finalize(Context& c);
+void ctx_refresh_dynamic(Context& c, bool force);
+void ctx_build_group(Context& c, int which);
+void ctx_assemble(Context& c, bool project, bool with_hessian);
+double ctx_total_energy(Context& c, double* per_energy);
+void ctx_apply_hessian_dev(Context& c, const double* x, double* y);
+void ctx_build_preconditioner(Context& c);
+void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev,
+             ys_step_stats* stats);
+void ctx_upload_domains(Context& c);
+uint64_t structure_checksum(Context& c, Structure& st, int64_t total_dofs);
+void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed,
+                       int64_t* n_pairs);
+void ctx_get_points(Context& c, int domain, double* out);
+
+// structure pieces reusable by the free-standing BSR path
+void build_structure_from_keys(Context& c, Structure& st, DevBuf<uint64_t>& keys,
+                               DevBuf<uint32_t>& payload, int64_t nkeys, int64_t total_dofs,
+                               const BlocksDev& blocks, bool build_assembly_plan);
+void build_spmv_plan(Context& c, Structure& st, const BlocksDev& blocks);
+void spmv_structure(Context& c, Structure& st, const BlocksDev& blocks, const double* x, double* y,
+                    bool accumulate, const PcgState* st_dev);
+
+BlocksDev blocks_view(Context& c);
+void drop_pcg_graph(Context& c);
+bool pcg_uses_conditional_graph(Context& c);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Number of SMs of the current device (grid sizing in multiples of the SM count).
+int sm_count();
+
+}  // namespace ys

@@ -1,0 +1,563 @@
+// ys_solver.cu — BSR SpMV and block-Jacobi PCG on the device.
+//
+// Reference: spmv_add / spmv_group_fixed (solver.cpp:10-82),
+// BlockJacobiPreconditioner::apply (138-146), pcg (151-200),
+// Engine::apply_hessian (engine.cpp:70-73), Engine::minimize_step (75-101).
+//
+// Layout: the upper-triangular blocks stay in the reference's storage
+// (shape groups, row-major values).  A per-block-row index lists every block
+// that touches the row — (r, c) directly and (c, r) transposed — so y is
+// produced row by row with no atomics: deterministic, one write per row, and
+// the second read of an off-diagonal block hits L2 (its rows are close in a
+// mesh ordering).  For pure 3x3 systems a 16-lane sub-warp owns a block row,
+// lanes stride over its entries and a fixed xor-butterfly reduces them.
+//
+// One PCG iteration = 3 kernels:
+//   k_spmv_dot : hp = (H_s + H_d) p, pHp partials, last CTA -> alpha / status
+//   k_update   : x += a p, r -= a hp, z = M^-1 r, |r|^2 and r.z partials,
+//                last CTA -> rel, history, convergence, beta
+//   k_pupdate  : p = z + beta p, and sets the graph's while-condition
+// captured once into a CUDA graph whose conditional WHILE node loops on the
+// device until the status word leaves 0 (no host round trip per iteration).
+#include <algorithm>
+#include <chrono>
+
+#include "ys_device.cuh"
+
+namespace ys {
+
+namespace {
+constexpr int kTB = 256;
+constexpr int kSW = 16;  // lanes per block row in the 3x3 SpMV
+}  // namespace
+
+struct SpmvDev {
+  const int32_t* rowptr;
+  const int32_t* ent;
+  const int32_t* row;
+  const int32_t* col;
+  const int8_t* br;
+  const int8_t* bc;
+  const int64_t* voff;
+  const double* values;
+};
+
+static SpmvDev spmv_dev(Structure& st) {
+  return SpmvDev{st.sp_rowptr.p, st.sp_ent.p, st.row.p, st.col.p, st.br.p, st.bc.p, st.voff.p, st.values.p};
+}
+
+// Block-level deterministic reduction of up to 3 doubles; result valid in thread 0.
+template <int K>
+__device__ __forceinline__ void block_reduce(double (&v)[K]) {
+  __shared__ double sm[K][kTB / 32];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sm[k][w] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a = 0.0;
+      for (int q = 0; q < int(blockDim.x >> 5); ++q) a += sm[k][q];
+      v[k] = a;
+    }
+  }
+}
+
+// Last-CTA election after every CTA stored its partials.
+__device__ __forceinline__ bool last_cta(unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  return last;
+}
+
+// Sums `n` partials (stride `stride`, K of them) in a fixed order inside the last CTA.
+template <int K>
+__device__ __forceinline__ void sum_partials(const double* part, int n, int stride, double (&out)[K]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += ((volatile const double*)part)[k * stride + q];
+  block_reduce<K>(out);
+}
+
+// --- SpMV row kernels -------------------------------------------------------
+
+__device__ __forceinline__ void acc33(const SpmvDev& S, int32_t j0, int32_t j1, int lane, const double* __restrict__ x,
+                                      double& a0, double& a1, double& a2) {
+  for (int32_t j = j0 + lane; j < j1; j += kSW) {
+    const uint32_t e = uint32_t(S.ent[j]);
+    const uint32_t u = e & 0x7fffffffu;
+    const double* v = S.values + 9 * int64_t(u);
+    if (e >> 31) {
+      const double* xo = x + S.row[u];
+      const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
+      a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
+      a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
+      a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
+    } else {
+      const double* xo = x + S.col[u];
+      const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
+      a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+      a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+      a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
+    }
+  }
+}
+
+// y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials.
+__global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+                                                const double* __restrict__ x, double* __restrict__ y, int accumulate,
+                                                PcgState* st, double* part) {
+  if (st && st->status) return;
+  const int lane = threadIdx.x % kSW;
+  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kSW;
+  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / kSW;
+  double dot[1] = {0.0};
+  for (int64_t R = sw0; R < nb; R += nsw) {
+    // every lane of a sub-warp sees the same R; sub-warp masks keep the
+    // reduction independent of the neighbouring sub-warp
+    const bool valid = true;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (valid) {
+      acc33(S0, S0.rowptr[R], S0.rowptr[R + 1], lane, x, a0, a1, a2);
+      if (has1) acc33(S1, S1.rowptr[R], S1.rowptr[R + 1], lane, x, a0, a1, a2);
+    }
+    const unsigned mask = ((1u << kSW) - 1u) << ((threadIdx.x & 31) & ~(kSW - 1));
+#pragma unroll
+    for (int off = kSW / 2; off > 0; off >>= 1) {
+      a0 += __shfl_xor_sync(mask, a0, off, kSW);
+      a1 += __shfl_xor_sync(mask, a1, off, kSW);
+      a2 += __shfl_xor_sync(mask, a2, off, kSW);
+    }
+    if (valid && lane == 0) {
+      double* yo = y + 3 * R;
+      if (accumulate) {
+        a0 += yo[0];
+        a1 += yo[1];
+        a2 += yo[2];
+      }
+      yo[0] = a0;
+      yo[1] = a1;
+      yo[2] = a2;
+      if (part) dot[0] += x[3 * R] * a0 + x[3 * R + 1] * a1 + x[3 * R + 2] * a2;
+    }
+  }
+  if (!part) return;
+  block_reduce<1>(dot);
+  if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
+  if (!last_cta(&st->counter1)) return;
+  double tot[1];
+  sum_partials<1>(part, gridDim.x, 0, tot);
+  if (threadIdx.x == 0) {
+    st->counter1 = 0;
+    const double php = tot[0];
+    st->php = php;
+    if (!isfinite(php) || php <= 0.0) {
+      if (php == 0.0) {
+        st->status = 2;  // stagnation on a semidefinite direction: break
+      } else {
+        st->status = 3;
+        st->fail_it = int(st->it);
+      }
+    } else {
+      st->alpha = st->rz / php;
+    }
+  }
+}
+
+// Generic shapes: one thread per block row.
+__device__ __forceinline__ void acc_gen(const SpmvDev& S, int64_t R, const double* __restrict__ x, double* acc) {
+  const int32_t j0 = S.rowptr[R], j1 = S.rowptr[R + 1];
+  for (int32_t j = j0; j < j1; ++j) {
+    const uint32_t e = uint32_t(S.ent[j]);
+    const uint32_t u = e & 0x7fffffffu;
+    const int r = S.br[u], c = S.bc[u];
+    const double* v = S.values + S.voff[u];
+    if (e >> 31) {
+      const double* xo = x + S.row[u];
+      for (int i = 0; i < c; ++i) {
+        double a = 0.0;
+        for (int k = 0; k < r; ++k) a += v[k * c + i] * xo[k];
+        acc[i] += a;
+      }
+    } else {
+      const double* xo = x + S.col[u];
+      for (int i = 0; i < r; ++i) {
+        double a = 0.0;
+        for (int k = 0; k < c; ++k) a += v[i * c + k] * xo[k];
+        acc[i] += a;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTB) k_spmv_gen(SpmvDev S0, SpmvDev S1, int has1, BlocksDev B,
+                                                  const double* __restrict__ x, double* __restrict__ y, int accumulate,
+                                                  PcgState* st, double* part) {
+  if (st && st->status) return;
+  double dot[1] = {0.0};
+  for (int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; R < B.nb; R += int64_t(gridDim.x) * blockDim.x) {
+    double acc[16];
+    const int rc = B.rc[R];
+    for (int i = 0; i < rc; ++i) acc[i] = 0.0;
+    acc_gen(S0, R, x, acc);
+    if (has1) acc_gen(S1, R, x, acc);
+    double* yo = y + B.start[R];
+    for (int i = 0; i < rc; ++i) {
+      const double v = accumulate ? yo[i] + acc[i] : acc[i];
+      yo[i] = v;
+      dot[0] += x[B.start[R] + i] * v;
+    }
+  }
+  if (!part) return;
+  block_reduce<1>(dot);
+  if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
+  if (!last_cta(&st->counter1)) return;
+  double tot[1];
+  sum_partials<1>(part, gridDim.x, 0, tot);
+  if (threadIdx.x == 0) {
+    st->counter1 = 0;
+    const double php = tot[0];
+    st->php = php;
+    if (!isfinite(php) || php <= 0.0) {
+      if (php == 0.0) st->status = 2;
+      else {
+        st->status = 3;
+        st->fail_it = int(st->it);
+      }
+    } else {
+      st->alpha = st->rz / php;
+    }
+  }
+}
+
+// --- PCG vector kernels -----------------------------------------------------
+
+template <int N>
+__device__ __forceinline__ void precond_apply(const double* __restrict__ M, const double* r, double* z) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) a += M[i * N + k] * r[k];
+    z[i] = a;
+  }
+}
+
+__device__ __forceinline__ void precond_apply_any(int rc, const double* M, const double* r, double* z) {
+  if (rc == 3) precond_apply<3>(M, r, z);
+  else if (rc == 9) precond_apply<9>(M, r, z);
+  else
+    for (int i = 0; i < rc; ++i) {
+      double a = 0.0;
+      for (int k = 0; k < rc; ++k) a += M[i * rc + k] * r[k];
+      z[i] = a;
+    }
+}
+
+// r = g; z = M^-1 r; p = z; x = 0; partials of g.g and r.z; last CTA -> gnorm, rz.
+__global__ void k_pcg_init(BlocksDev B, int uniform3, const double* __restrict__ g, const double* __restrict__ minv,
+                           double* r, double* z, double* p, double* x, PcgState* st, double* part, double* hist) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < B.nb; b += int64_t(gridDim.x) * blockDim.x) {
+    const int rc = uniform3 ? 3 : B.rc[b];
+    const int64_t s0 = uniform3 ? 3 * b : B.start[b];
+    const double* M = minv + (uniform3 ? 9 * b : B.voff[b]);
+    double rr[16], zz[16];
+    for (int i = 0; i < rc; ++i) {
+      rr[i] = g[s0 + i];
+      r[s0 + i] = rr[i];
+      x[s0 + i] = 0.0;
+    }
+    precond_apply_any(rc, M, rr, zz);
+    for (int i = 0; i < rc; ++i) {
+      z[s0 + i] = zz[i];
+      p[s0 + i] = zz[i];
+      v[0] += rr[i] * rr[i];
+      v[1] += rr[i] * zz[i];
+    }
+  }
+  block_reduce<2>(v);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = v[0];
+    part[gridDim.x + blockIdx.x] = v[1];
+  }
+  if (!last_cta(&st->counter2)) return;
+  double tot[2];
+  sum_partials<2>(part, gridDim.x, gridDim.x, tot);
+  if (threadIdx.x == 0) {
+    st->counter2 = 0;
+    st->gnorm = sqrt(tot[0]);
+    st->rz = tot[1];
+    st->it = 0;
+    st->rel = 0.0;
+    st->fail_it = -1;
+    if (st->gnorm == 0.0) {
+      st->status = 1;  // converged with x = 0 (solver.cpp:156-159)
+    } else {
+      st->status = st->max_iter > 0 ? 0 : 5;
+      st->rel = 1.0;
+      hist[0] = 1.0;
+    }
+  }
+}
+
+// x += a p; r -= a hp; z = M^-1 r; partials of r.r and r.z; last CTA -> rel,
+// history, convergence test, beta (solver.cpp:170-197).
+__global__ void __launch_bounds__(kTB) k_update(BlocksDev B, int uniform3, const double* __restrict__ minv,
+                                                double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                                const double* __restrict__ p, const double* __restrict__ hp,
+                                                PcgState* st, double* part, double* hist) {
+  if (st->status) return;
+  const double a = st->alpha;
+  double v[2] = {0.0, 0.0};
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < B.nb; b += int64_t(gridDim.x) * blockDim.x) {
+    if (uniform3) {
+      const int64_t s0 = 3 * b;
+      double rr[3], zz[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        x[s0 + i] += a * p[s0 + i];
+        rr[i] = r[s0 + i] - a * hp[s0 + i];
+        r[s0 + i] = rr[i];
+      }
+      precond_apply<3>(minv + 9 * b, rr, zz);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        z[s0 + i] = zz[i];
+        v[0] += rr[i] * rr[i];
+        v[1] += rr[i] * zz[i];
+      }
+    } else {
+      const int rc = B.rc[b];
+      const int64_t s0 = B.start[b];
+      double rr[16], zz[16];
+      for (int i = 0; i < rc; ++i) {
+        x[s0 + i] += a * p[s0 + i];
+        rr[i] = r[s0 + i] - a * hp[s0 + i];
+        r[s0 + i] = rr[i];
+      }
+      precond_apply_any(rc, minv + B.voff[b], rr, zz);
+      for (int i = 0; i < rc; ++i) {
+        z[s0 + i] = zz[i];
+        v[0] += rr[i] * rr[i];
+        v[1] += rr[i] * zz[i];
+      }
+    }
+  }
+  block_reduce<2>(v);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = v[0];
+    part[gridDim.x + blockIdx.x] = v[1];
+  }
+  if (!last_cta(&st->counter2)) return;
+  double tot[2];
+  sum_partials<2>(part, gridDim.x, gridDim.x, tot);
+  if (threadIdx.x == 0) {
+    st->counter2 = 0;
+    const long long it = st->it;
+    const double rel = sqrt(tot[0]) / st->gnorm;
+    st->it = it + 1;
+    st->rel = rel;
+    if (it + 1 < st->hist_cap) hist[it + 1] = rel;
+    if (!isfinite(rel)) {
+      st->status = 4;
+      st->fail_it = int(it);
+    } else if (rel <= st->tol) {
+      st->status = 1;
+    } else if (it + 1 >= st->max_iter) {
+      st->status = 5;
+    } else {
+      st->beta = tot[1] / st->rz;
+      st->rz = tot[1];
+    }
+  }
+}
+
+__global__ void k_pupdate(int64_t s, const double* __restrict__ z, double* __restrict__ p, PcgState* st,
+                          cudaGraphConditionalHandle h, int use_cond) {
+  const int status = st->status;
+  if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, status == 0 ? 1u : 0u);
+  if (status) return;
+  const double b = st->beta;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = z[i] + b * p[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+
+void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, double* y, bool accumulate,
+                 PcgState* st, double* part, int grid) {
+  const bool has1 = s1 && s1->n_blocks > 0;
+  const bool fast = c.uniform3 && s0.all33 && (!has1 || s1->all33);
+  SpmvDev d0 = spmv_dev(s0);
+  SpmvDev d1 = has1 ? spmv_dev(*s1) : d0;
+  if (fast)
+    k_spmv33<<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
+  else
+    k_spmv_gen<<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, blocks_view(c), x, y, accumulate ? 1 : 0, st,
+                                           part);
+  YS_LAUNCH_CHECK();
+}
+
+void ctx_apply_hessian_dev(Context& c, const double* x, double* y) {
+  spmv_launch(c, c.S[0], &c.S[1], x, y, true, nullptr, nullptr, std::max(1, sm_count() * 8));
+}
+
+static void launch_iteration(Context& c, int grid, cudaGraphConditionalHandle h, bool use_cond) {
+  PcgState* st = c.pcg.p;
+  spmv_launch(c, c.S[0], &c.S[1], c.p.p, c.hp.p, false, st, c.partials.p, grid);
+  k_update<<<grid, kTB, 0, c.stream>>>(blocks_view(c), c.uniform3 ? 1 : 0, c.minv.p, c.DX.p, c.r.p, c.z.p, c.p.p,
+                                       c.hp.p, st, c.partials.p, c.hist.p);
+  YS_LAUNCH_CHECK();
+  k_pupdate<<<grid, kTB, 0, c.stream>>>(c.s, c.z.p, c.p.p, st, h, use_cond ? 1 : 0);
+  YS_LAUNCH_CHECK();
+}
+
+static bool build_conditional_graph(Context& c, int grid) {
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  }
+  launch_iteration(c, grid, h, true);
+  cudaGraph_t out = nullptr;
+  if (cudaStreamEndCapture(c.stream, &out) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraphExec_t exec = nullptr;
+  if (cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  }
+  c.pcg_graph = g;
+  c.pcg_exec = exec;
+  c.pcg_cond = true;
+  return true;
+}
+
+static void build_chunk_graph(Context& c, int grid, int chunk) {
+  cudaGraph_t g = nullptr;
+  YS_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < chunk; ++k) launch_iteration(c, grid, cudaGraphConditionalHandle{}, false);
+  YS_CUDA(cudaStreamEndCapture(c.stream, &g));
+  YS_CUDA(cudaGraphInstantiate(&c.pcg_exec, g, 0));
+  c.pcg_graph = g;
+  c.pcg_cond = false;
+}
+
+void drop_pcg_graph(Context& c) {
+  if (c.pcg_exec) cudaGraphExecDestroy(c.pcg_exec);
+  if (c.pcg_graph) cudaGraphDestroy(c.pcg_graph);
+  c.pcg_exec = nullptr;
+  c.pcg_graph = nullptr;
+}
+
+int pcg_grid(Context& c) { return std::max(1, sm_count() * 8); }
+
+void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev, ys_step_stats* stats) {
+  cudaStream_t s = c.stream;
+  const int grid = pcg_grid(c);
+  c.r.resize(c.s);
+  c.z.resize(c.s);
+  c.p.resize(c.s);
+  c.hp.resize(c.s);
+  c.pcg.resize(1);
+  c.partials.resize(std::max<size_t>(c.partials.n, size_t(2 * grid)));
+  const int64_t hist_cap = std::min<int64_t>(max_iter, int64_t(1) << 22) + 2;
+  c.hist.resize(std::max<size_t>(c.hist.n, size_t(hist_cap)));
+  if (x_dev != c.DX.p) fail(YS_ERR_INTERNAL, "pcg: solution must live in the step buffer");
+  (void)g_dev;
+  PcgState init{};
+  init.tol = tol;
+  init.max_iter = max_iter;
+  init.hist_cap = int64_t(c.hist.n);
+  YS_CUDA(cudaMemcpyAsync(c.pcg.p, &init, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  k_pcg_init<<<grid, kTB, 0, s>>>(blocks_view(c), c.uniform3 ? 1 : 0, c.G.p, c.minv.p, c.r.p, c.z.p, c.p.p, c.DX.p,
+                                  c.pcg.p, c.partials.p, c.hist.p);
+  YS_LAUNCH_CHECK();
+
+  // graph cache key: every pointer / flag the captured launches bake in
+  Structure& s0 = c.S[0];
+  Structure& s1 = c.S[1];
+  auto P = [](const void* q) { return uint64_t(uintptr_t(q)); };
+  std::vector<uint64_t> key = {P(s0.sp_rowptr.p), P(s0.sp_ent.p), P(s0.values.p), P(s0.row.p), P(s0.col.p),
+                               P(s0.br.p), P(s0.bc.p), P(s0.voff.p), P(s1.sp_rowptr.p), P(s1.sp_ent.p),
+                               P(s1.values.p), P(s1.row.p), P(s1.col.p), P(s1.br.p), P(s1.bc.p), P(s1.voff.p),
+                               P(c.DX.p), P(c.r.p), P(c.z.p), P(c.p.p), P(c.hp.p), P(c.minv.p), P(c.pcg.p),
+                               P(c.partials.p), P(c.hist.p),
+                               uint64_t(s1.n_blocks > 0) | (uint64_t(s0.all33) << 1) | (uint64_t(s1.all33) << 2),
+                               uint64_t(grid), uint64_t(c.s)};
+  if (!c.pcg_exec || c.pcg_key != key) {
+    drop_pcg_graph(c);
+    if (!build_conditional_graph(c, grid)) build_chunk_graph(c, grid, 8);
+    c.pcg_key = key;
+  }
+  PcgState fin{};
+  if (c.pcg_cond) {
+    YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+    YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+  } else {
+    for (;;) {
+      YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      YS_CUDA(cudaStreamSynchronize(s));
+      if (fin.status) break;
+      YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+    }
+  }
+  c.launches += 2 + 3 * fin.it;
+  c.hist_count = fin.status == 1 && fin.it == 0 && fin.gnorm == 0.0 ? 0 : fin.it + 1;
+  if (fin.status == 3)
+    fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
+                               " (non-finite or negative curvature)");
+  if (fin.status == 4)
+    fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) + " (non-finite residual)");
+  if (stats) {
+    stats->pcg_iterations = fin.it;
+    stats->pcg_converged = fin.status == 1 ? 1 : 0;
+    stats->pcg_residual = (fin.gnorm == 0.0) ? 0.0 : fin.rel;
+  }
+}
+
+bool pcg_uses_conditional_graph(Context& c) { return c.pcg_cond; }
+
+}  // namespace ys

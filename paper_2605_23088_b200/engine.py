@@ -1,0 +1,444 @@
+"""Python mirror of relsim::Engine over the C-ABI (engine.hpp:27-80).
+
+`Engine` drives one context of a C-ABI implementation: the B200 library by
+default, or — for parity tests only — the CPU oracle / the reference build,
+which export the same functions.  Method names, argument meaning and raised
+exception classes follow the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import (YS_POINTS_AFFINE, YS_POINTS_FIXED, YS_POINTS_FREE, YS_PROJECT_FULL,  # noqa: F401
+                   YS_PROJECT_REDUCED, StepStats, check)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _ip32(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(-1)
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64)).reshape(-1)
+
+
+@dataclass
+class Step:
+    dx: np.ndarray | None
+    pcg_iterations: int
+    pcg_residual: float
+    pcg_converged: bool
+    regularized_blocks: int
+    assemble_seconds: float
+    solve_seconds: float
+
+
+@dataclass
+class HessianStructure:
+    groups: np.ndarray  # n x 5 {rows, cols, coord_start, count, value_start}
+    row: np.ndarray
+    col: np.ndarray
+    values: np.ndarray
+    checksum: int
+    total_dofs: int
+
+    def to_dense(self) -> np.ndarray:
+        """BlockSparseHessian::to_dense (assembly.cpp:91-104)."""
+        s = self.total_dofs
+        d = np.zeros((s, s))
+        for rows, cols, cs, cnt, vs in self.groups:
+            for k in range(cnt):
+                r, c = self.row[cs + k], self.col[cs + k]
+                b = self.values[vs + k * rows * cols: vs + (k + 1) * rows * cols].reshape(rows, cols)
+                d[r:r + rows, c:c + cols] += b
+                if r != c:
+                    d[c:c + cols, r:r + rows] += b.T
+        return d
+
+    def blocks(self):
+        """Yields (rows, cols, row, col, block) in storage order."""
+        for rows, cols, cs, cnt, vs in self.groups:
+            for k in range(cnt):
+                yield (int(rows), int(cols), int(self.row[cs + k]), int(self.col[cs + k]),
+                       self.values[vs + k * rows * cols: vs + (k + 1) * rows * cols].reshape(rows, cols))
+
+
+class Engine:
+    def __init__(self, backend: str = "gpu", device: int = 0):
+        if backend == "gpu":
+            self.lib = _lib.gpu_library()
+        elif backend == "oracle":
+            self.lib = _lib.oracle_library()
+        elif backend == "reference":
+            self.lib = _lib.reference_library()
+        else:
+            raise ValueError(backend)
+        self.backend = backend
+        self.f = self.lib.fns
+        h = C.c_void_p()
+        st = self.f["create"](C.byref(h), device)
+        if st != 0:
+            raise _lib.CudaError(f"{self.lib.path.name}: context creation failed (status {st}); "
+                                 "the B200 path needs an sm_100 device")
+        self.ctx = h
+        self.targets: list[tuple[int, int]] = []
+        self.energy_names: list[str] = []
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.f["destroy"](self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, status):
+        check(self.lib, self.ctx, status)
+
+    # ---------------- scene side ----------------
+    def add_target(self, instances: int, rc: int, values=None) -> int:
+        tid = C.c_int32()
+        self._c(self.f["add_target"](self.ctx, int(instances), int(rc), C.byref(tid)))
+        self.targets.append((int(instances), int(rc)))
+        if values is not None:
+            self.set_target_values(tid.value, values)
+        return tid.value
+
+    def set_target_values(self, tid: int, values):
+        v = _f64(values)
+        self._c(self.f["set_target_values"](self.ctx, tid, _dp(v)))
+
+    def get_target_values(self, tid: int) -> np.ndarray:
+        n, rc = self.targets[tid]
+        out = np.zeros(n * rc)
+        self._c(self.f["get_target_values"](self.ctx, tid, _dp(out)))
+        return out
+
+    def total_dofs(self) -> int:
+        s = C.c_int64()
+        self._c(self.f["total_dofs"](self.ctx, C.byref(s)))
+        return s.value
+
+    def add_points(self, kind: int, n: int, target_a: int = -1, target_b: int = -1, v2b=None,
+                   rest=None) -> int:
+        did = C.c_int32()
+        vb = _i64(v2b if v2b is not None else np.zeros(0))
+        rs = _f64(rest if rest is not None else np.zeros(0))
+        self._c(self.f["add_points"](self.ctx, kind, int(n), target_a, target_b, _ip64(vb), _dp(rs),
+                                     C.byref(did)))
+        return did.value
+
+    def get_points(self, domain: int, n: int) -> np.ndarray:
+        out = np.zeros(3 * n)
+        self._c(self.f["get_points"](self.ctx, domain, _dp(out)))
+        return out.reshape(n, 3)
+
+    def add_point_union(self, domains) -> int:
+        d = np.ascontiguousarray(np.asarray(domains, dtype=np.int32))
+        uid = C.c_int32()
+        self._c(self.f["add_point_union"](self.ctx, len(d), _ip32(d), C.byref(uid)))
+        return uid.value
+
+    def add_pair_set(self, union_id: int, dynamic: bool = True) -> int:
+        pid = C.c_int32()
+        self._c(self.f["add_pair_set"](self.ctx, union_id, 1 if dynamic else 0, C.byref(pid)))
+        return pid.value
+
+    def set_pairs(self, pairset: int, pairs):
+        p = _i64(pairs)
+        self._c(self.f["set_pairs"](self.ctx, pairset, len(p) // 2, _ip64(p)))
+
+    def pair_count(self, pairset: int) -> int:
+        n = C.c_int64()
+        self._c(self.f["pair_count"](self.ctx, pairset, C.byref(n)))
+        return n.value
+
+    def refresh_pairs(self, pairset: int, dhat: float, child_is_fixed=None) -> int:
+        n = C.c_int64()
+        if child_is_fixed is None:
+            fx = None
+        else:
+            a = np.ascontiguousarray(np.asarray(child_is_fixed, dtype=np.int32))
+            fx = _ip32(a)
+        self._c(self.f["refresh_pairs"](self.ctx, pairset, float(dhat), fx, C.byref(n)))
+        return n.value
+
+    def _eid(self, name: str, out: C.c_int32) -> int:
+        self.energy_names.append(name)
+        return out.value
+
+    def add_stable_neo_hookean(self, pos_target: int, t2v, rest, youngs: float, poisson: float,
+                               weight: float = 1.0, via_deformation_gradient: bool = False) -> int:
+        t = _i64(t2v)
+        r = _f64(rest)
+        e = C.c_int32()
+        self._c(self.f["add_stable_neo_hookean"](self.ctx, pos_target, len(t) // 4, _ip64(t), _dp(r),
+                                                 float(youngs), float(poisson), float(weight),
+                                                 1 if via_deformation_gradient else 0, C.byref(e)))
+        return self._eid("stable_neo_hookean", e)
+
+    def add_point_point_barrier(self, pairset: int, dhat: float, kappa: float, weight: float = 1.0,
+                                mode: int = YS_PROJECT_FULL) -> int:
+        e = C.c_int32()
+        self._c(self.f["add_point_point_barrier"](self.ctx, pairset, float(dhat), float(kappa), float(weight),
+                                                  mode, C.byref(e)))
+        return self._eid("point_point", e)
+
+    def add_repulsive(self, pairset: int, weight: float = 1.0, mode: int = YS_PROJECT_FULL) -> int:
+        e = C.c_int32()
+        self._c(self.f["add_repulsive"](self.ctx, pairset, float(weight), mode, C.byref(e)))
+        return self._eid("repulsive", e)
+
+    def add_inertia(self, domain: int, mass, x_tilde) -> int:
+        m = _f64(mass)
+        x = _f64(x_tilde)
+        e = C.c_int32()
+        self._c(self.f["add_inertia"](self.ctx, domain, _dp(m), _dp(x), C.byref(e)))
+        return self._eid("inertia", e)
+
+    def set_inertia_anchor(self, energy: int, x_tilde):
+        x = _f64(x_tilde)
+        self._c(self.f["set_inertia_anchor"](self.ctx, energy, _dp(x)))
+
+    def add_affine_orthogonality(self, amat_target: int, stiffness: float, weight: float = 1.0) -> int:
+        e = C.c_int32()
+        self._c(self.f["add_affine_orthogonality"](self.ctx, amat_target, float(stiffness), float(weight),
+                                                   C.byref(e)))
+        return self._eid("affine_orthogonality", e)
+
+    def add_bending(self, pos_target: int, h2v, rest, stiffness: float, weight: float = 1.0) -> int:
+        h = _i64(h2v)
+        r = _f64(rest)
+        e = C.c_int32()
+        self._c(self.f["add_bending"](self.ctx, pos_target, len(h) // 4, _ip64(h), _dp(r), float(stiffness),
+                                      float(weight), C.byref(e)))
+        return self._eid("bending", e)
+
+    # ---------------- engine side ----------------
+    def finalize(self):
+        self._c(self.f["finalize"](self.ctx))
+        self.s = self.total_dofs()
+
+    def refresh_dynamic(self):
+        self._c(self.f["refresh_dynamic"](self.ctx))
+
+    def dynamic_stale(self) -> bool:
+        v = C.c_int32()
+        self._c(self.f["dynamic_stale"](self.ctx, C.byref(v)))
+        return bool(v.value)
+
+    def assemble(self, project: bool = True, with_hessian: bool = True):
+        self._c(self.f["assemble"](self.ctx, 1 if project else 0, 1 if with_hessian else 0))
+
+    def gradient(self) -> np.ndarray:
+        g = np.zeros(self.s)
+        self._c(self.f["get_gradient"](self.ctx, _dp(g)))
+        return g
+
+    def total_energy(self) -> float:
+        e = C.c_double()
+        self._c(self.f["total_energy"](self.ctx, C.byref(e)))
+        return e.value
+
+    def energy_totals(self) -> np.ndarray:
+        out = np.zeros(len(self.energy_names))
+        self._c(self.f["energy_totals"](self.ctx, _dp(out)))
+        return out
+
+    def apply_hessian(self, x, y=None) -> np.ndarray:
+        xv = _f64(x)
+        yv = np.zeros(self.s) if y is None else _f64(y).copy()
+        self._c(self.f["apply_hessian"](self.ctx, _dp(xv), _dp(yv)))
+        return yv
+
+    def minimize_step(self, tol: float = 1e-6, max_iter: int = -1, want_dx: bool = True) -> Step:
+        st = StepStats()
+        dx = np.zeros(self.s) if want_dx else None
+        self._c(self.f["minimize_step"](self.ctx, float(tol), int(max_iter),
+                                        _dp(dx) if want_dx else None, C.byref(st)))
+        return Step(dx, st.pcg_iterations, st.pcg_residual, bool(st.pcg_converged), st.regularized_blocks,
+                    st.assemble_seconds, st.solve_seconds)
+
+    def split_per_target(self, flat: np.ndarray) -> list[np.ndarray]:
+        out, off = [], 0
+        for n, rc in self.targets:
+            out.append(flat[off:off + n * rc])
+            off += n * rc
+        return out
+
+    def pcg_history(self) -> np.ndarray:
+        cnt = C.c_int64()
+        cap = 1 << 20
+        h = np.zeros(cap)
+        self._c(self.f["pcg_history"](self.ctx, cap, _dp(h), C.byref(cnt)))
+        return h[:min(cnt.value, cap)].copy()
+
+    def gather_targets(self) -> np.ndarray:
+        x = np.zeros(self.s)
+        self._c(self.f["gather_targets"](self.ctx, _dp(x)))
+        return x
+
+    def scatter_targets(self, x):
+        xv = _f64(x)
+        if len(xv) != self.s:
+            raise _lib.ValidationError("scatter_targets: length mismatch")
+        self._c(self.f["scatter_targets"](self.ctx, _dp(xv)))
+
+    def step_targets(self, alpha: float) -> float:
+        m = C.c_double()
+        self._c(self.f["step_targets"](self.ctx, float(alpha), C.byref(m)))
+        return m.value
+
+    # ---------------- introspection ----------------
+    def hessian(self, which: int) -> HessianStructure:
+        ng, nb, nv = C.c_int64(), C.c_int64(), C.c_int64()
+        cs = C.c_uint64()
+        self._c(self.f["hessian_info"](self.ctx, which, C.byref(ng), C.byref(nb), C.byref(nv), C.byref(cs)))
+        groups = np.zeros(5 * ng.value, dtype=np.int64)
+        row = np.zeros(nb.value, dtype=np.int64)
+        col = np.zeros(nb.value, dtype=np.int64)
+        vals = np.zeros(nv.value)
+        if ng.value:
+            self._c(self.f["hessian_groups"](self.ctx, which, _ip64(groups)))
+        if nb.value:
+            self._c(self.f["hessian_coords"](self.ctx, which, _ip64(row), _ip64(col)))
+        if nv.value:
+            self._c(self.f["hessian_values"](self.ctx, which, _dp(vals)))
+        return HessianStructure(groups.reshape(-1, 5), row, col, vals, cs.value, self.s)
+
+    def static_hessian(self) -> HessianStructure:
+        return self.hessian(0)
+
+    def dynamic_hessian(self) -> HessianStructure:
+        return self.hessian(1)
+
+    def dense_hessian(self) -> np.ndarray:
+        """Engine::dense_hessian (engine.cpp:62)."""
+        return self.static_hessian().to_dense() + self.dynamic_hessian().to_dense()
+
+    def energy_info(self, e: int) -> dict:
+        n, k, w, d = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        self._c(self.f["energy_info"](self.ctx, e, C.byref(n), C.byref(k), C.byref(w), C.byref(d)))
+        return {"instances": n.value, "kappa": k.value, "width": w.value, "dynamic": bool(d.value)}
+
+    def energy_slots(self, e: int):
+        info = self.energy_info(e)
+        cnt = info["instances"] * info["kappa"]
+        idx = np.zeros(cnt, dtype=np.int64)
+        ln = np.zeros(cnt, dtype=np.int32)
+        col = np.zeros(cnt, dtype=np.int32)
+        if cnt:
+            self._c(self.f["energy_slots"](self.ctx, e, _ip64(idx), _ip32(ln), _ip32(col)))
+        k = max(info["kappa"], 1)
+        return idx.reshape(-1, k), ln.reshape(-1, k), col.reshape(-1, k)
+
+    def energy_compressed_sizes(self, e: int) -> np.ndarray:
+        n = self.energy_info(e)["instances"]
+        m = np.zeros(n, dtype=np.int32)
+        if n:
+            self._c(self.f["energy_compressed_sizes"](self.ctx, e, _ip32(m)))
+        return m
+
+    def diag_blocks(self) -> list[np.ndarray]:
+        total = sum(n * rc * rc for n, rc in self.targets)
+        buf = np.zeros(total)
+        self._c(self.f["diag_blocks"](self.ctx, _dp(buf)))
+        out, off = [], 0
+        for n, rc in self.targets:
+            for _ in range(n):
+                out.append(buf[off:off + rc * rc].reshape(rc, rc))
+                off += rc * rc
+        return out
+
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        self._c(self.f["device_bytes"](self.ctx, C.byref(b)))
+        return b.value
+
+    def set_profiling(self, on: bool):
+        if self.lib.has("set_profiling"):
+            self._c(self.f["set_profiling"](self.ctx, 1 if on else 0))
+
+    def stage_times(self):
+        ms = np.zeros(8)
+        cnt = np.zeros(2, dtype=np.int64)
+        self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
+        return ms, int(cnt[0])
+
+
+class BlockSystem:
+    """Free-standing BlockSparseHessian + spmv_add + pcg (solver.hpp:13-48)."""
+
+    def __init__(self, engine: Engine, total_dofs: int, coords):
+        self.eng = engine
+        self.s = int(total_dofs)
+        c = _i64(coords)
+        bid = C.c_int32()
+        engine._c(engine.f["bsr_build"](engine.ctx, self.s, len(c) // 4, _ip64(c), C.byref(bid)))
+        self.id = bid.value
+        ng, nb, nv = C.c_int64(), C.c_int64(), C.c_int64()
+        cs = C.c_uint64()
+        engine._c(engine.f["bsr_info"](engine.ctx, self.id, C.byref(ng), C.byref(nb), C.byref(nv), C.byref(cs)))
+        self.checksum = cs.value
+        self.groups = np.zeros(5 * ng.value, dtype=np.int64)
+        self.row = np.zeros(nb.value, dtype=np.int64)
+        self.col = np.zeros(nb.value, dtype=np.int64)
+        self.n_values = nv.value
+        if ng.value:
+            engine._c(engine.f["bsr_groups"](engine.ctx, self.id, _ip64(self.groups)))
+            engine._c(engine.f["bsr_coords"](engine.ctx, self.id, _ip64(self.row), _ip64(self.col)))
+        self.groups = self.groups.reshape(-1, 5)
+
+    def value_offset(self, rows, cols, row, col) -> int:
+        for r, c, cs, cnt, vs in self.groups:
+            if r != rows or c != cols:
+                continue
+            lo, hi = cs, cs + cnt
+            while lo < hi:
+                mid = (lo + hi) // 2
+                if (self.row[mid], self.col[mid]) < (row, col):
+                    lo = mid + 1
+                else:
+                    hi = mid
+            if lo < cs + cnt and self.row[lo] == row and self.col[lo] == col:
+                return int(vs + (lo - cs) * r * c)
+            break
+        raise _lib.InternalError(f"block ({row},{col}) not present")
+
+    def set_values(self, values):
+        v = _f64(values)
+        self.eng._c(self.eng.f["bsr_set_values"](self.eng.ctx, self.id, _dp(v)))
+
+    def spmv(self, x, y=None) -> np.ndarray:
+        xv = _f64(x)
+        if len(xv) != self.s:
+            raise _lib.ValidationError(f"spmv: vector length {len(xv)} != system size {self.s}")
+        yv = np.zeros(self.s) if y is None else _f64(y).copy()
+        self.eng._c(self.eng.f["bsr_spmv"](self.eng.ctx, self.id, _dp(xv), _dp(yv)))
+        return yv
+
+    def pcg(self, g, block_size: int, tol: float, max_iter: int):
+        gv = _f64(g)
+        x = np.zeros(self.s)
+        it, rel, conv = C.c_int64(), C.c_double(), C.c_int32()
+        self.eng._c(self.eng.f["bsr_pcg"](self.eng.ctx, self.id, int(block_size), _dp(gv), float(tol),
+                                          int(max_iter), _dp(x), C.byref(it), C.byref(rel), C.byref(conv)))
+        return x, it.value, rel.value, bool(conv.value)
