@@ -228,6 +228,17 @@ int ys_bsr_pcg(ys_context* ctx, int32_t bsr, int32_t bs, const double* g, double
  * ------------------------------------------------------------------------ */
 int ys_set_profiling(ys_context* ctx, int32_t enabled);
 int ys_stage_times(ys_context* ctx, double* ms, int64_t* counts);
+/* Scene::bump_dynamic_epoch (scene.hpp:190): forces the next minimize_step
+ * to rebuild the dynamic structure, as every refresh_dynamic_pairs does. */
+int ys_bump_dynamic_epoch(ys_context* ctx);
+/* The cudaStream_t every kernel of the context is launched on (for CUDA-event
+ * timing by the caller). */
+int ys_stream(ys_context* ctx, void** stream);
+/* Times one kernel class alone: reps launches bracketed by CUDA events on the
+ * context stream.  which: 0 = PCG SpMV (static + dynamic, fused pHp),
+ * 1 = assembly gather of the static group, 2 = local evaluation of all
+ * energies.  avg_ms per launch; bytes = algorithmic bytes per launch. */
+int ys_time_kernel(ys_context* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);
 
 #ifdef __cplusplus
 }

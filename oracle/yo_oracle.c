@@ -1853,6 +1853,18 @@ int yo_diag_blocks(yo_context* c, double* out) {
   API_END;
 }
 
+int yo_bump_dynamic_epoch(yo_context* c) {
+  API_BEGIN(c);
+  c->epoch++;
+  API_END;
+}
+
+int yo_stream(yo_context* c, void** stream) {
+  API_BEGIN(c);
+  *stream = NULL;
+  API_END;
+}
+
 /* --- free-standing BSR ---------------------------------------------------- */
 int yo_bsr_build(yo_context* c, int64_t s, int64_t n, const int64_t* coords, int32_t* id) {
   API_BEGIN(c);

@@ -129,11 +129,14 @@ _SIGS = {
     "bsr_pcg": [_P, _I32, _I32, _PD, _D, _I64, _PD, _PI64, _PD, _PI32],
     "set_profiling": [_P, _I32],
     "stage_times": [_P, _PD, _PI64],
+    "bump_dynamic_epoch": [_P],
+    "stream": [_P, C.POINTER(C.c_void_p)],
+    "time_kernel": [_P, _I32, _I32, _PD, _PD],
 }
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
-OPTIONAL = {"set_profiling", "stage_times", "device_bytes"}
+OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream"}
 
 
 class Library:

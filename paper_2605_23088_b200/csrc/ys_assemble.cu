@@ -530,11 +530,8 @@ static void record(Context& c, int idx) {
   if (c.profiling) YS_CUDA(cudaEventRecord(c.ev[idx], c.stream));
 }
 
-void ctx_assemble(Context& c, bool project, bool with_hessian) {
-  if (c.seen_epoch != c.epoch)
-    fail(YS_ERR_VALIDATION, "dynamic structures are stale after resize_dynamic; call refresh_dynamic()");
+void ctx_eval_all(Context& c, bool project, bool with_hessian) {
   cudaStream_t s = c.stream;
-  record(c, 1);
   for (size_t id = 0; id < c.energies.size(); ++id) {
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
@@ -559,21 +556,31 @@ void ctx_assemble(Context& c, bool project, bool with_hessian) {
     YS_LAUNCH_CHECK();
     ++c.launches;
   }
-  record(c, 2);
-  if (with_hessian) {
-    for (int w = 0; w < 2; ++w) {
-      Structure& st = c.S[w];
-      for (auto& g : st.groups) {
-        const int rc = int(g[0] * g[1]);
-        const int64_t cnt = g[3];
-        if (cnt == 0) continue;
-        k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc,
-                                                      st.voff.p, st.values.p);
-        YS_LAUNCH_CHECK();
-        ++c.launches;
-      }
+}
+
+void ctx_gather_all(Context& c) {
+  cudaStream_t s = c.stream;
+  for (int w = 0; w < 2; ++w) {
+    Structure& st = c.S[w];
+    for (auto& g : st.groups) {
+      const int rc = int(g[0] * g[1]);
+      const int64_t cnt = g[3];
+      if (cnt == 0) continue;
+      k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc, st.voff.p,
+                                                    st.values.p);
+      YS_LAUNCH_CHECK();
+      ++c.launches;
     }
   }
+}
+
+void ctx_assemble(Context& c, bool project, bool with_hessian) {
+  if (c.seen_epoch != c.epoch)
+    fail(YS_ERR_VALIDATION, "dynamic structures are stale after resize_dynamic; call refresh_dynamic()");
+  record(c, 1);
+  ctx_eval_all(c, project, with_hessian);
+  record(c, 2);
+  if (with_hessian) ctx_gather_all(c);
   record(c, 3);
   ctx_block_rows(c, with_hessian);
   record(c, 4);

@@ -50,6 +50,8 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
                  PcgState* st, double* part, int grid);
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
+void ctx_gather_all(Context& c);
+void ctx_eval_all(Context& c, bool project, bool with_hessian);
 
 namespace {
 
@@ -1098,6 +1100,58 @@ int ys_bsr_pcg(ys_context* c, int32_t id, int32_t bs, const double* g, double to
     if (iters) *iters = st.pcg_iterations;
     if (rel) *rel = st.pcg_residual;
     if (conv) *conv = st.pcg_converged;
+  });
+}
+
+int ys_bump_dynamic_epoch(ys_context* c) {
+  return guarded(c, [&] { ++c->epoch; });
+}
+
+int ys_stream(ys_context* c, void** stream) {
+  return guarded(c, [&] { *stream = reinterpret_cast<void*>(c->stream); });
+}
+
+int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
+  return guarded(c, [&] {
+    require_finalized(*c);
+    if (reps < 1) reps = 1;
+    cudaStream_t s = c->stream;
+    double alg = 0.0;
+    auto launch = [&]() {
+      if (which == 0) {
+        spmv_launch(*c, c->S[0], &c->S[1], c->p.p, c->hp.p, false, nullptr, nullptr, pcg_grid(*c));
+      } else if (which == 1) {
+        ctx_gather_all(*c);
+        ctx_block_rows(*c, true);
+      } else {
+        ctx_eval_all(*c, true, true);
+      }
+    };
+    if (which == 0) {
+      c->p.resize(c->s);
+      c->hp.resize(c->s);
+      YS_CUDA(cudaMemcpyAsync(c->p.p, c->G.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      // 8 r c (values) + 8 (two int32 coords) per upper block, 16 s per SpMV
+      for (int w = 0; w < 2; ++w)
+        for (auto& g : c->S[w].groups) alg += double(g[3]) * (8.0 * g[0] * g[1] + 8.0);
+      alg += 16.0 * double(c->s);
+    } else if (which == 1) {
+      // per instance 8 sum(r c) + 4 #dest + 8 width + 4 kappa; once 8 nvalues + 8 s + 8 diag
+      for (auto& e : c->energies) {
+        if (e.n == 0 || e.kappa == 0) continue;
+        alg += 8.0 * double(e.hsize) + 4.0 * double(e.ndest) + 8.0 * double(e.n) * e.width + 4.0 * double(e.n) * e.kappa;
+      }
+      alg += 8.0 * double(c->S[0].n_values + c->S[1].n_values) + 8.0 * double(c->s) + 8.0 * double(c->diag_vals);
+    }
+    launch();  // warm
+    YS_CUDA(cudaEventRecord(c->ev[7], s));
+    for (int k = 0; k < reps; ++k) launch();
+    YS_CUDA(cudaEventRecord(c->ev[8], s));
+    YS_CUDA(cudaEventSynchronize(c->ev[8]));
+    float ms = 0.f;
+    YS_CUDA(cudaEventElapsedTime(&ms, c->ev[7], c->ev[8]));
+    *avg_ms = double(ms) / reps;
+    if (bytes) *bytes = alg;
   });
 }
 

@@ -156,10 +156,11 @@ __global__ void k_lower_bound_blocks(const uint32_t* keys, int64_t n, const int3
                                      int32_t* seg) {
   const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b > nb) return;
-  if (b == nb) {
+  if (b == nb && bstart) {
     seg[b] = int32_t(n);
     return;
   }
+  // block-id keys: rowptr[nb] = first sentinel (diagonal blocks emit one entry)
   const uint32_t v = bstart ? uint32_t(bstart[b]) : uint32_t(b);
   int64_t lo = 0, hi = n;
   while (lo < hi) {

@@ -377,6 +377,19 @@ class Engine:
         if self.lib.has("set_profiling"):
             self._c(self.f["set_profiling"](self.ctx, 1 if on else 0))
 
+    def bump_dynamic_epoch(self):
+        self._c(self.f["bump_dynamic_epoch"](self.ctx))
+
+    def stream_handle(self) -> int:
+        h = C.c_void_p()
+        self._c(self.f["stream"](self.ctx, C.byref(h)))
+        return h.value or 0
+
+    def time_kernel(self, which: int, reps: int = 20):
+        ms, b = C.c_double(), C.c_double()
+        self._c(self.f["time_kernel"](self.ctx, which, reps, C.byref(ms), C.byref(b)))
+        return ms.value, b.value
+
     def stage_times(self):
         ms = np.zeros(8)
         cnt = np.zeros(2, dtype=np.int64)

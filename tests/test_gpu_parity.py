@@ -1,0 +1,253 @@
+"""GPU parity: the B200 library (through its C-ABI) against the CPU oracle on
+identical scenes.  Bars (BASELINE.json north_star):
+bit-exact slot tables, compressed sizes, shape groups, coordinates and
+structure checksum; energy, gradient, Hessian blocks, diagonal blocks and PCG
+solutions within 1e-9 relative (max|diff| / max|ref| per array); identical PCG
+iteration counts."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2605_23088_b200 import NumericalError, ValidationError
+from paper_2605_23088_b200.engine import YS_PROJECT_FULL, YS_PROJECT_REDUCED, BlockSystem, Engine
+from fixtures import ContactScene, random_system, rel, tet_scene
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def both(build):
+    out = []
+    for backend in ("gpu", "oracle"):
+        eng = Engine(backend)
+        handles = build(eng)
+        eng.finalize()
+        out.append((eng, handles))
+    return out
+
+
+def assert_structures_equal(g: Engine, o: Engine):
+    for which in (0, 1):
+        hg, ho = g.hessian(which), o.hessian(which)
+        assert np.array_equal(hg.groups, ho.groups), f"groups differ ({which})"
+        assert np.array_equal(hg.row, ho.row) and np.array_equal(hg.col, ho.col), f"coords differ ({which})"
+        assert hg.checksum == ho.checksum, f"checksum differs ({which})"
+
+
+def assert_tables_equal(g: Engine, o: Engine):
+    for e in range(len(g.energy_names)):
+        ig, io = g.energy_info(e), o.energy_info(e)
+        assert ig == io
+        for a, b in zip(g.energy_slots(e), o.energy_slots(e)):
+            assert np.array_equal(a, b), f"slot tables of energy {e} differ"
+        assert np.array_equal(g.energy_compressed_sizes(e), o.energy_compressed_sizes(e))
+
+
+def assert_values_close(g: Engine, o: Engine, tol=TOL):
+    assert rel(g.gradient(), o.gradient()) <= tol
+    for which in (0, 1):
+        vg, vo = g.hessian(which).values, o.hessian(which).values
+        assert vg.shape == vo.shape
+        if vo.size:
+            assert rel(vg, vo) <= tol, f"H values ({which}) rel {rel(vg, vo)}"
+    dg, do = g.diag_blocks(), o.diag_blocks()
+    assert rel(np.concatenate([b.ravel() for b in dg]), np.concatenate([b.ravel() for b in do])) <= tol
+
+
+def full_check(g, o, project=True, tol=TOL):
+    assert_tables_equal(g, o)
+    assert_structures_equal(g, o)
+    g.assemble(project)
+    o.assemble(project)
+    assert_values_close(g, o, tol)
+    assert abs(g.total_energy() - o.total_energy()) <= 1e-12 * max(1.0, abs(o.total_energy()))
+
+
+@pytest.mark.parametrize("energy", ["repulsive", "pp"])
+@pytest.mark.parametrize("project", [True, False])
+def test_contact_scene_mixed_pairs(energy, project):
+    pairs = [(0, 3 + 1), (1, 2), (3 + 0, 3 + 3), (0, 3 + 1), (3 + 0, 3 + 1), (2, 3 + 2)]
+
+    def build(eng):
+        cs = ContactScene(eng, 3, 2, 4, seed=12)
+        if energy == "repulsive":
+            eng.add_repulsive(cs.pp, 1.0)
+        else:
+            eng.add_point_point_barrier(cs.pp, 6.0, 5.0, 1.0)
+        cs.set_pairs(pairs)
+        return cs
+
+    (g, _), (o, _) = both(build)
+    full_check(g, o, project)
+    # compressed sizes {6, 12, 15, 24} incl. the same-body merge (test_assembly.cpp:120-161)
+    assert set(g.energy_compressed_sizes(0).tolist()) == {6, 12, 15, 24}
+
+
+def test_contact_scene_with_fixed_branch_and_resize():
+    def build(eng):
+        cs = ContactScene(eng, 4, 2, 5, seed=8, n_fixed=3)
+        eng.add_point_point_barrier(cs.pp, 8.0, 3.0, 0.5)
+        cs.set_pairs([(0, cs.fixed_index(1)), (cs.abd_index(2), cs.fixed_index(0)), (1, cs.abd_index(4))])
+        return cs
+
+    (g, cg), (o, co) = both(build)
+    full_check(g, o)
+    assert set(g.energy_compressed_sizes(0).tolist()) == {3, 12, 15}
+    # resize_dynamic -> stale -> refresh (engine.cpp:41-60)
+    for eng, cs in ((g, cg), (o, co)):
+        cs.set_pairs([(2, cs.abd_index(0)), (cs.abd_index(1), cs.fixed_index(2))])
+        with pytest.raises(ValidationError, match="stale"):
+            eng.assemble()
+        eng.refresh_dynamic()
+    full_check(g, o)
+    # resize to zero
+    for eng, cs in ((g, cg), (o, co)):
+        cs.set_pairs([])
+        eng.refresh_dynamic()
+    full_check(g, o)
+    assert g.dynamic_hessian().values.size == 0
+
+
+@pytest.mark.parametrize("via_f", [False, True])
+@pytest.mark.parametrize("seed", [21, 22])
+def test_stable_neo_hookean(via_f, seed):
+    def build(eng):
+        t, t2v, rest = tet_scene(eng, 6, seed, 0.15)
+        eng.add_stable_neo_hookean(t, t2v, rest, 9.88e3, 0.35, 1.0, via_f)
+        return t
+
+    (g, _), (o, _) = both(build)
+    for project in (False, True):
+        full_check(g, o, project)
+
+
+def test_bending_and_inertia_cloth():
+    from paper_2605_23088_b200.scene import hinges, make_grid_cloth
+
+    def build(eng):
+        rng = np.random.default_rng(3)
+        v, tris = make_grid_cloth(6, 5, 0.1)
+        v = v + 0.03 * rng.uniform(-1, 1, v.shape)
+        t = eng.add_target(len(v), 3, v)
+        d = eng.add_points(0, len(v), t)
+        eng.add_bending(t, hinges(tris).reshape(-1), v, 0.055, 0.7)
+        eng.add_inertia(d, rng.uniform(0.5, 2.0, len(v)), v + 0.01)
+        return t
+
+    (g, _), (o, _) = both(build)
+    full_check(g, o, True)
+    full_check(g, o, False)
+
+
+def test_affine_orthogonality_and_abd_inertia():
+    def build(eng):
+        cs = ContactScene(eng, 2, 3, 6, seed=6)
+        eng.add_affine_orthogonality(cs.t_A, 1e4, 0.3)
+        rng = np.random.default_rng(61)
+        eng.add_inertia(cs.d_abd, rng.uniform(0.5, 2.0, 6), rng.uniform(-1, 1, (6, 3)))
+        eng.add_inertia(cs.d_free, np.ones(2), np.zeros((2, 3)))
+        return cs
+
+    (g, _), (o, _) = both(build)
+    full_check(g, o, True)
+    full_check(g, o, False)
+
+
+def test_minimize_step_matches_oracle():
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+
+    cfg = SimConfig.from_dict(configs.c3())
+    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    for s in sims:
+        configs.jitter_targets(s, 0.002)
+        s.begin_frame()
+        s.refresh_dynamic_pairs()
+    assert sims[0].pair_count() == sims[1].pair_count() > 0
+    g, o = sims[0].eng, sims[1].eng
+    assert_structures_equal(g, o)
+    sg = g.minimize_step(1e-4)
+    so = o.minimize_step(1e-4)
+    assert sg.pcg_iterations == so.pcg_iterations
+    assert sg.pcg_converged == so.pcg_converged
+    assert rel(sg.dx, so.dx) <= TOL
+    assert rel(g.pcg_history(), o.pcg_history()) <= 1e-6
+
+
+def test_block_system_spmv_and_pcg():
+    for nb, bs, seed in ((10, 3, 1), (25, 3, 2), (8, 9, 3), (30, 3, 11)):
+        s, coords, vals = random_system(nb, bs, 0.3, seed)
+        systems = []
+        for backend in ("gpu", "oracle"):
+            eng = Engine(backend)
+            bsys = BlockSystem(eng, s, np.asarray(coords).reshape(-1))
+            v = np.zeros(bsys.n_values)
+            for (r, c), b in vals.items():
+                off = bsys.value_offset(bs, bs, r, c)
+                v[off:off + bs * bs] = b.ravel()
+            bsys.set_values(v)
+            systems.append((eng, bsys))
+        (eg, g), (eo, o) = systems
+        assert g.checksum == o.checksum
+        x = np.random.default_rng(seed).uniform(-1, 1, s)
+        yg, yo = g.spmv(x), o.spmv(x)
+        assert rel(yg, yo) <= 1e-12
+        rhs = np.random.default_rng(seed + 3).uniform(-1, 1, s)
+        for pre in (bs, 0):
+            xg, itg, rg, cg = g.pcg(rhs, pre, 1e-8, s)
+            xo, ito, ro, co = o.pcg(rhs, pre, 1e-8, s)
+            assert itg == ito and cg == co
+            assert rel(xg, xo) <= 1e-9
+
+
+def test_numerical_errors_match_reference_wording():
+    # singular / non-finite diagonal block names the DoF range (test_solver.cpp:176-194)
+    s, coords, vals = random_system(2, 3, 0.0, 5)
+    for backend in ("gpu", "oracle"):
+        eng = Engine(backend)
+        bsys = BlockSystem(eng, s, np.asarray(coords).reshape(-1))
+        v = np.zeros(bsys.n_values)
+        v[0:9] = np.eye(3).ravel()
+        v[9:18] = np.nan
+        bsys.set_values(v)
+        with pytest.raises(NumericalError, match=r"\[3, 6\)"):
+            bsys.pcg(np.ones(s), 3, 1e-8, 10)
+        # PCG divergence names the iteration
+        v[9:18] = (-np.eye(3)).ravel()
+        v[0:9] = (-np.eye(3)).ravel()
+        bsys.set_values(v)
+        with pytest.raises(NumericalError, match="iteration"):
+            bsys.pcg(np.ones(s), 0, 1e-8, 10)
+
+
+def test_refresh_pairs_bit_exact():
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+
+    cfg = SimConfig.from_dict(configs.c3())
+    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    for s in sims:
+        configs.jitter_targets(s, 0.004, seed=99)
+    n = [s.refresh_dynamic_pairs() for s in sims]
+    assert n[0] == n[1] > 0
+    sims[0].eng.refresh_dynamic()
+    sims[1].eng.refresh_dynamic()
+    assert_tables_equal(sims[0].eng, sims[1].eng)
+    assert_structures_equal(sims[0].eng, sims[1].eng)
+
+
+def test_newton_frames_positions():
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+
+    cfg = SimConfig.from_dict(configs.c1())
+    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    for frame in range(3):
+        reps = [s.step() for s in sims]
+        assert reps[0].iterations == reps[1].iterations
+        assert reps[0].pcg_iterations == reps[1].pcg_iterations
+        pg = np.concatenate([p.ravel() for p in sims[0].positions()])
+        po = np.concatenate([p.ravel() for p in sims[1].positions()])
+        assert rel(pg, po) <= TOL
+        assert sims[0].pair_count() == sims[1].pair_count()

@@ -1,0 +1,38 @@
+"""Quick device smoke timing of minimize_step on C1..C5 (development aid)."""
+import sys
+import time
+
+import numpy as np
+
+from paper_2605_23088_b200 import configs
+from paper_2605_23088_b200.scene import SimConfig, Simulation
+
+names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+for name in names:
+    t0 = time.perf_counter()
+    cfg = SimConfig.from_dict(configs.CONFIGS[name]())
+    sim = Simulation(cfg, backend="gpu")
+    t1 = time.perf_counter()
+    sp = 0.1 * (0.025 if name == "c1" else 0.01)
+    configs.jitter_targets(sim, sp)
+    sim.begin_frame()
+    n = sim.refresh_dynamic_pairs()
+    t2 = time.perf_counter()
+    eng = sim.eng
+    eng.set_profiling(True)
+    times = []
+    for k in range(4):
+        eng.bump_dynamic_epoch()
+        a = time.perf_counter()
+        st = eng.minimize_step(cfg.pcg_tol, -1, want_dx=False)
+        times.append(time.perf_counter() - a)
+    ms, launches = eng.stage_times()
+    sp_ms, sp_b = eng.time_kernel(0, 50)
+    as_ms, as_b = eng.time_kernel(1, 10)
+    ev_ms, _ = eng.time_kernel(2, 10)
+    print(f"{name}: s={eng.s} pairs={n} build={t1-t0:.2f}s pairs_t={t2-t1:.2f}s "
+          f"step_ms={[round(1e3*t,2) for t in times]} pcg_it={st.pcg_iterations} conv={st.pcg_converged} "
+          f"res={st.pcg_residual:.2e} stages(ms) refresh={ms[0]:.3f} eval={ms[1]:.3f} gather={ms[2]:.3f} "
+          f"rows={ms[3]:.3f} pcg={ms[4]:.3f} total={ms[6]:.3f} launches={launches}", flush=True)
+    print(f"   spmv {sp_ms*1e3:.1f}us {sp_b/sp_ms/1e6:.0f} GB/s | assembly {as_ms*1e3:.1f}us {as_b/as_ms/1e6:.0f} GB/s | "
+          f"eval {ev_ms*1e3:.1f}us | dev bytes {eng.device_bytes()/1e9:.2f} GB", flush=True)
