@@ -104,6 +104,8 @@ int ys_add_pair_set(ys_context* ctx, int32_t union_id, int32_t dynamic, int32_t*
  * may only be set before ys_finalize. */
 int ys_set_pairs(ys_context* ctx, int32_t pairset, int64_t n, const int64_t* pairs);
 int ys_pair_count(ys_context* ctx, int32_t pairset, int64_t* n);
+/* The current pair table (2*n union-global indices). */
+int ys_get_pairs(ys_context* ctx, int32_t pairset, int64_t* pairs);
 /* Simulation::refresh_dynamic_pairs (sim.cpp:456-484) on the device: every
  * pair (i in child ca, j in child cb), ca < cb, not both fixed, with squared
  * distance < dhat, in the reference's loop order; then resize_dynamic. */

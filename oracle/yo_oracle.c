@@ -1429,6 +1429,13 @@ int yo_pair_count(yo_context* c, int32_t ps, int64_t* n) {
   API_END;
 }
 
+int yo_get_pairs(yo_context* c, int32_t ps, int64_t* out) {
+  API_BEGIN(c);
+  if (ps < 0 || ps >= c->nps) fail(c, YS_ERR_DECL, "unknown pair set");
+  memcpy(out, c->ps[ps].pairs, sizeof(int64_t) * (size_t)(2 * c->ps[ps].n));
+  API_END;
+}
+
 /* Simulation::refresh_dynamic_pairs (sim.cpp:456-484) */
 int yo_refresh_pairs(yo_context* c, int32_t ps, double dhat, const int32_t* child_fixed, int64_t* out_n) {
   API_BEGIN(c);

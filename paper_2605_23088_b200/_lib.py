@@ -90,6 +90,7 @@ _SIGS = {
     "add_pair_set": [_P, _I32, _I32, _PI32],
     "set_pairs": [_P, _I32, _I64, _PI64],
     "pair_count": [_P, _I32, _PI64],
+    "get_pairs": [_P, _I32, _PI64],
     "refresh_pairs": [_P, _I32, _D, _PI32, _PI64],
     "add_stable_neo_hookean": [_P, _I32, _I64, _PI64, _PD, _D, _D, _D, _I32, _PI32],
     "add_point_point_barrier": [_P, _I32, _D, _D, _D, _I32, _PI32],

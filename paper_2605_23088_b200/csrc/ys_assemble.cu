@@ -171,7 +171,87 @@ __global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* _
   for (int k = 0; k < 9; ++k) go[k] = g[k];
 }
 
-// Inertia and pair energies: one 3-vector delta, linear in the compressed DoFs.
+// Inertia of free points: one 3x3 block m I (projection: max(m, 0) I).
+__global__ void k_eval_inertia_free(EnergyDev E, const double* __restrict__ X, int project, int want_h,
+                                    double* __restrict__ hc, double* __restrict__ gc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  const double* q = X + E.dom.startA + 3 * i;
+  const double* xt = E.anchor + 3 * i;
+  const double m = E.cdata[i];
+  double* go = gc + E.gbase + 3 * i;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) go[k] = m * (q[k] - xt[k]);
+  if (!want_h) return;
+  const double d = (project && !(m > 0.0)) ? 0.0 : m;
+  double* h = hc + E.hbase + 9 * i;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) h[k] = (k % 4 == 0) ? d : 0.0;
+}
+
+// Pair energies over unions of free / fixed points (kappa_u == 1).
+__global__ void k_eval_pair_free(EnergyDev E, const double* __restrict__ X, int project, int want_h,
+                                 double* __restrict__ hc, double* __restrict__ gc, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double p[2][3];
+  int32_t gs[2];
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    int64_t loc;
+    const int br = union_decode(E.uni, E.pairs[2 * i + l], &loc);
+    const DomainDev& d = E.uni.child[br];
+    if (d.kind == YS_POINTS_FREE) {
+      gs[l] = int32_t(d.startA + 3 * loc);
+      const double* q = X + gs[l];
+      p[l][0] = q[0]; p[l][1] = q[1]; p[l][2] = q[2];
+    } else {
+      gs[l] = -1;
+      const double* q = d.fixed + 3 * loc;
+      p[l][0] = q[0]; p[l][1] = q[1]; p[l][2] = q[2];
+    }
+  }
+  double dl[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dl[k] = p[1][k] - p[0][k];
+  const double d = dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2];
+  const PairParams PP{E.prm[0], E.prm[1], E.prm[2], E.kind == K_REPULSIVE};
+  double b, b1, b2;
+  const int st = pair_b(d, PP, &b, &b1, &b2);
+  if (st) atomicOr(err, st == 1 ? kErrLog : kErrDiv);
+  double* go = gc + inst_goff(E, i);
+  int o = 0;
+#pragma unroll
+  for (int l = 0; l < 2; ++l) {
+    if (gs[l] < 0) continue;
+    const double sg = l == 0 ? -2.0 * b1 : 2.0 * b1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) go[o + k] = sg * dl[k];
+    o += 3;
+  }
+  if (!want_h) return;
+  double P[9];
+  proj_rank1_3(2.0 * b1, 4.0 * b2, dl, d, project != 0, P);
+  double* h = hc + inst_hoff(E, i);
+  const int nfree = (gs[0] >= 0) + (gs[1] >= 0);
+  if (nfree == 2 && gs[0] == gs[1]) {  // both ends on one vertex: merged, rho = 0
+#pragma unroll
+    for (int k = 0; k < 9; ++k) h[k] = 0.0;
+  } else if (nfree == 2) {  // (0,0) = P, (0,1) = -P (symmetric, orientation-free), (1,1) = P
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      h[k] = P[k];
+      h[9 + k] = -P[k];
+      h[18 + k] = P[k];
+    }
+  } else if (nfree == 1) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) h[k] = P[k];
+  }
+}
+
+// Inertia over affine points and pair energies over unions with affine
+// bodies: one 3-vector delta, linear in the compressed DoFs.
 __global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int project, int want_h,
                              double* __restrict__ hc, double* __restrict__ gc, int* err) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -486,12 +566,14 @@ __device__ __forceinline__ void block_row_work(int64_t b, const BlocksDev& B, co
   bflag[b] = jacobi_block_inverse<N>(blk, minv + B.voff[b]);
 }
 
-// One launch per target (uniform block size N within a target).
+// One launch per block-size class (block ids from the class list, or all
+// blocks of a uniform layout).
 template <int N>
-__global__ void k_block_rows(BlocksDev B, int64_t b0, int64_t nb, GroupView S0, GroupView S1, double* G,
-                             double* diag, double* minv, int32_t* bflag, int want_h) {
-  const int64_t b = b0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (b >= b0 + nb) return;
+__global__ void k_block_rows(BlocksDev B, const int32_t* __restrict__ list, int64_t nb, GroupView S0, GroupView S1,
+                             double* G, double* diag, double* minv, int32_t* bflag, int want_h) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  const int64_t b = list ? list[q] : q;
   block_row_work<N>(b, B, S0, S1, G, diag, minv, bflag, want_h);
 }
 
@@ -549,9 +631,20 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
       case K_ORTHO:
         k_eval_ortho<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
         break;
+      case K_INERTIA:
+        if (c.domains[e.domain].kind == YS_POINTS_FREE)
+          k_eval_inertia_free<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
+        else
+          k_eval_point<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                          c.errflag.p);
+        break;
       default:
-        k_eval_point<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
-                                                        c.errflag.p);
+        if (E.uni.kappa_u == 1)
+          k_eval_pair_free<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                              c.errflag.p);
+        else
+          k_eval_point<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                          c.errflag.p);
     }
     YS_LAUNCH_CHECK();
     ++c.launches;
@@ -580,7 +673,12 @@ void ctx_assemble(Context& c, bool project, bool with_hessian) {
   record(c, 1);
   ctx_eval_all(c, project, with_hessian);
   record(c, 2);
-  if (with_hessian) ctx_gather_all(c);
+  if (with_hessian) {
+    ctx_gather_all(c);
+  } else {  // Engine::assemble zeroes both stores and the diagonal (engine.cpp:50-53)
+    for (int w = 0; w < 2; ++w) c.S[w].values.zero(c.stream);
+    c.diag.zero(c.stream);
+  }
   record(c, 3);
   ctx_block_rows(c, with_hessian);
   record(c, 4);
@@ -593,19 +691,27 @@ void ctx_block_rows(Context& c, bool want_h) {
   const BlocksDev B = blocks_view(c);
   const GroupView S0 = group_view(c.S[0], true), S1 = group_view(c.S[1], true);
   const int wh = want_h ? 1 : 0;
-  for (const Target& t : c.targets) {
-    if (t.n == 0) continue;
-    const unsigned g = grid_for(t.n, 128);
-    switch (t.rc) {
-      case 1: k_block_rows<1><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 2: k_block_rows<2><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 3: k_block_rows<3><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 4: k_block_rows<4><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 6: k_block_rows<6><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 9: k_block_rows<9><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      case 12: k_block_rows<12><<<g, 128, 0, c.stream>>>(B, t.block0, t.n, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); break;
-      default: fail(YS_ERR_INTERNAL, "unsupported target block size");
+  for (size_t k = 0; k < c.rc_classes.size(); ++k) {
+    const int32_t* list = c.rc_classes.size() == 1 ? nullptr : c.rc_lists[k].p;
+    const int64_t nb = c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[k].n);
+    if (nb == 0) continue;
+    const unsigned g = grid_for(nb, 128);
+#define YS_ROWS(N)                                                                                            \
+  case N:                                                                                                     \
+    k_block_rows<N><<<g, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); \
+    break;
+    switch (c.rc_classes[k]) {
+      YS_ROWS(1)
+      YS_ROWS(2)
+      YS_ROWS(3)
+      YS_ROWS(4)
+      YS_ROWS(6)
+      YS_ROWS(9)
+      YS_ROWS(12)
+      default:
+        fail(YS_ERR_INTERNAL, "unsupported target block size");
     }
+#undef YS_ROWS
     YS_LAUNCH_CHECK();
     ++c.launches;
   }

@@ -51,6 +51,7 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
 void ctx_gather_all(Context& c);
+
 void ctx_eval_all(Context& c, bool project, bool with_hessian);
 
 namespace {
@@ -210,6 +211,18 @@ void ctx_finalize(Context& c) {
       vo += int64_t(t.rc) * t.rc;
       for (int k = 0; k < t.rc; ++k) d2b[t.start + i * t.rc + k] = int32_t(b);
     }
+  c.rc_classes.clear();
+  c.rc_lists.clear();
+  for (int32_t r : brc)
+    if (std::find(c.rc_classes.begin(), c.rc_classes.end(), r) == c.rc_classes.end()) c.rc_classes.push_back(r);
+  std::sort(c.rc_classes.begin(), c.rc_classes.end());
+  for (int32_t r : c.rc_classes) {
+    std::vector<int32_t> lst;
+    for (int64_t q = 0; q < nb; ++q)
+      if (brc[q] == r) lst.push_back(int32_t(q));
+    c.rc_lists.emplace_back();
+    c.rc_lists.back().upload(lst, s);
+  }
   c.bstart.upload(bstart, s);
   c.brc.upload(brc, s);
   c.bvoff.upload(bvoff, s);
@@ -395,6 +408,9 @@ void ys_destroy(ys_context* c) {
   cudaStreamSynchronize(c->stream);
   drop_pcg_graph(*c);
   for (auto& sub : c->subs) drop_pcg_graph(*sub);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto& sub : c->subs)
+    if (sub->pinned) cudaFreeHost(sub->pinned);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   c->subs.clear();
@@ -556,6 +572,14 @@ int ys_pair_count(ys_context* c, int32_t ps, int64_t* n) {
   return guarded(c, [&] {
     if (ps < 0 || ps >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown pair set");
     *n = c->pairsets[ps].n;
+  });
+}
+
+int ys_get_pairs(ys_context* c, int32_t ps, int64_t* out) {
+  return guarded(c, [&] {
+    if (ps < 0 || ps >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown pair set");
+    const PairSet& p = c->pairsets[ps];
+    std::copy(p.h_pairs.begin(), p.h_pairs.end(), out);
   });
 }
 

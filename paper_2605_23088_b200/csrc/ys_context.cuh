@@ -113,7 +113,14 @@ struct Structure {
   DevBuf<int32_t> diag_uid;     // NB: unique block index of the (b,b) block, -1 if absent
   // SpMV plan: full (both triangle) row lists over block rows.
   DevBuf<int32_t> sp_rowptr;    // NB + 1
-  DevBuf<int32_t> sp_ent;       // uid | (transposed << 31)
+  DevBuf<int32_t> sp_ent;       // uid | (transposed << 31), row-sorted
+  DevBuf<int32_t> sp_oth;       // first DoF of the other block side of entry j
+  DevBuf<int32_t> sp_pos_n;     // per uid: position of its (r, c) entry
+  DevBuf<int32_t> sp_pos_t;     // per uid: position of its transposed entry, -1 on the diagonal
+  // 3x3 structures: upper-storage row plan (normal blocks are contiguous in u)
+  DevBuf<int32_t> nrow;         // NB + 1: first unique block of each block row
+  DevBuf<int32_t> trow;         // NB + 1: first transposed entry of each block row
+  DevBuf<int2> tlist;           // (u, row DoF) of off-diagonal blocks, sorted by column block
   int32_t max_row_len = 0;
   uint64_t checksum = 0;
   bool checksum_valid = false;
@@ -179,6 +186,11 @@ struct Context {
   DevBuf<uint32_t> p_in, gk_in, gk_out, gp_in;
   DevBuf<int32_t> flags, incl, ghead, heads;
   DevBuf<unsigned char> grpbuf;
+  DevBuf<unsigned char> cnt4, ex4;   // per-instance counts / offsets of non-uniform energies
+  DevBuf<unsigned char> summary;     // device-side structure summary
+  void* pinned = nullptr;            // 64 KiB pinned staging for small D2H copies
+  std::vector<int32_t> rc_classes;   // distinct target block sizes
+  std::vector<DevBuf<int32_t>> rc_lists;  // block ids per rc class (non-uniform layouts)
 
   // profiling
   bool profiling = false;

@@ -20,6 +20,8 @@
 // captured once into a CUDA graph whose conditional WHILE node loops on the
 // device until the status word leaves 0 (no host round trip per iteration).
 #include <algorithm>
+#include <string>
+#include <cstdlib>
 #include <chrono>
 
 #include "ys_device.cuh"
@@ -32,18 +34,22 @@ constexpr int kSW = 16;  // lanes per block row in the 3x3 SpMV
 }  // namespace
 
 struct SpmvDev {
-  const int32_t* rowptr;
-  const int32_t* ent;
-  const int32_t* row;
-  const int32_t* col;
+  const int32_t* rowptr;  // NB + 1
+  const int32_t* ent;     // uid | transposed << 31, row-sorted
+  const int32_t* oth;     // first DoF of the other block side per entry
   const int8_t* br;
   const int8_t* bc;
   const int64_t* voff;
-  const double* values;
+  const double* values;   // reference layout (upper blocks, u sorted by (row, col))
+  const int32_t* col;     // per uid
+  const int32_t* nrow;    // 3x3 plan: NB + 1
+  const int32_t* trow;    // 3x3 plan: NB + 1
+  const int2* tlist;      // 3x3 plan: (u, row DoF) per transposed entry
 };
 
 static SpmvDev spmv_dev(Structure& st) {
-  return SpmvDev{st.sp_rowptr.p, st.sp_ent.p, st.row.p, st.col.p, st.br.p, st.bc.p, st.voff.p, st.values.p};
+  return SpmvDev{st.sp_rowptr.p, st.sp_ent.p, st.sp_oth.p, st.br.p, st.bc.p, st.voff.p, st.values.p,
+                 st.col.p, st.nrow.p, st.trow.p, st.tlist.p};
 }
 
 // Block-level deterministic reduction of up to 3 doubles; result valid in thread 0.
@@ -95,54 +101,57 @@ __device__ __forceinline__ void sum_partials(const double* part, int n, int stri
 
 // --- SpMV row kernels -------------------------------------------------------
 
-__device__ __forceinline__ void acc33(const SpmvDev& S, int32_t j0, int32_t j1, int lane, const double* __restrict__ x,
-                                      double& a0, double& a1, double& a2) {
-  for (int32_t j = j0 + lane; j < j1; j += kSW) {
-    const uint32_t e = uint32_t(S.ent[j]);
-    const uint32_t u = e & 0x7fffffffu;
-    const double* v = S.values + 9 * int64_t(u);
-    if (e >> 31) {
-      const double* xo = x + S.row[u];
-      const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
-      a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
-      a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
-      a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
-    } else {
-      const double* xo = x + S.col[u];
-      const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
-      a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
-      a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
-      a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
-    }
+// Block row R of a 3x3 upper-storage structure: its own blocks (R, c) are the
+// contiguous u range [nrow[R], nrow[R+1]) (y_R += B x_c); the blocks (r, R),
+// r < R, come from tlist (y_R += B^T x_r) and are mostly L2 hits — row r
+// streamed them moments earlier.
+template <int SW>
+__device__ __forceinline__ void acc33(const SpmvDev& S, int64_t R, int lane, const double* __restrict__ x, double& a0,
+                                      double& a1, double& a2) {
+  const int32_t n0 = S.nrow[R], n1 = S.nrow[R + 1];
+  const int32_t t0 = S.trow[R], t1 = S.trow[R + 1];
+  for (int32_t u = n0 + lane; u < n1; u += SW) {
+    const double* __restrict__ v = S.values + 9 * int64_t(u);
+    const double* __restrict__ xo = x + S.col[u];
+    const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
+    a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+    a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+    a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
+  }
+  for (int32_t j = t0 + lane; j < t1; j += SW) {
+    const int2 t = S.tlist[j];
+    const double* __restrict__ v = S.values + 9 * int64_t(t.x);
+    const double* __restrict__ xo = x + t.y;
+    const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
+    a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
+    a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
+    a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
   }
 }
 
-// y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials.
+// y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials
+// reduced to pHp and alpha by the last CTA.
+template <int SW>
 __global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
                                                 const double* __restrict__ x, double* __restrict__ y, int accumulate,
                                                 PcgState* st, double* part) {
   if (st && st->status) return;
-  const int lane = threadIdx.x % kSW;
-  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kSW;
-  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / kSW;
+  const int lane = threadIdx.x % SW;
+  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
+  const unsigned mask = (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u)) << ((threadIdx.x & 31) & ~(SW - 1));
   double dot[1] = {0.0};
   for (int64_t R = sw0; R < nb; R += nsw) {
-    // every lane of a sub-warp sees the same R; sub-warp masks keep the
-    // reduction independent of the neighbouring sub-warp
-    const bool valid = true;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (valid) {
-      acc33(S0, S0.rowptr[R], S0.rowptr[R + 1], lane, x, a0, a1, a2);
-      if (has1) acc33(S1, S1.rowptr[R], S1.rowptr[R + 1], lane, x, a0, a1, a2);
-    }
-    const unsigned mask = ((1u << kSW) - 1u) << ((threadIdx.x & 31) & ~(kSW - 1));
+    acc33<SW>(S0, R, lane, x, a0, a1, a2);
+    if (has1) acc33<SW>(S1, R, lane, x, a0, a1, a2);
 #pragma unroll
-    for (int off = kSW / 2; off > 0; off >>= 1) {
-      a0 += __shfl_xor_sync(mask, a0, off, kSW);
-      a1 += __shfl_xor_sync(mask, a1, off, kSW);
-      a2 += __shfl_xor_sync(mask, a2, off, kSW);
+    for (int off = SW / 2; off > 0; off >>= 1) {
+      a0 += __shfl_xor_sync(mask, a0, off, SW);
+      a1 += __shfl_xor_sync(mask, a1, off, SW);
+      a2 += __shfl_xor_sync(mask, a2, off, SW);
     }
-    if (valid && lane == 0) {
+    if (lane == 0) {
       double* yo = y + 3 * R;
       if (accumulate) {
         a0 += yo[0];
@@ -178,51 +187,69 @@ __global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1
   }
 }
 
-// Generic shapes: one thread per block row.
-__device__ __forceinline__ void acc_gen(const SpmvDev& S, int64_t R, const double* __restrict__ x, double* acc) {
+// Generic shapes: one warp per block row of size RC (launched per block-size
+// class), lanes over the row's entries, fixed xor-butterfly reduction.
+template <int RC>
+__device__ __forceinline__ void acc_gen(const SpmvDev& S, int64_t R, int lane, const double* __restrict__ x,
+                                        double (&acc)[RC]) {
   const int32_t j0 = S.rowptr[R], j1 = S.rowptr[R + 1];
-  for (int32_t j = j0; j < j1; ++j) {
+  for (int32_t j = j0 + lane; j < j1; j += 32) {
     const uint32_t e = uint32_t(S.ent[j]);
     const uint32_t u = e & 0x7fffffffu;
     const int r = S.br[u], c = S.bc[u];
     const double* v = S.values + S.voff[u];
-    if (e >> 31) {
-      const double* xo = x + S.row[u];
-      for (int i = 0; i < c; ++i) {
-        double a = 0.0;
-        for (int k = 0; k < r; ++k) a += v[k * c + i] * xo[k];
-        acc[i] += a;
+    const double* xo = x + S.oth[j];
+    if (e >> 31) {  // block (other, R): y_R += B^T x_other, B is r x RC
+      for (int k = 0; k < r; ++k) {
+        const double xk = xo[k];
+#pragma unroll
+        for (int i = 0; i < RC; ++i) acc[i] += v[k * RC + i] * xk;
       }
-    } else {
-      const double* xo = x + S.col[u];
-      for (int i = 0; i < r; ++i) {
-        double a = 0.0;
-        for (int k = 0; k < c; ++k) a += v[i * c + k] * xo[k];
-        acc[i] += a;
+    } else {  // block (R, other): y_R += B x_other, B is RC x c
+      for (int k = 0; k < c; ++k) {
+        const double xk = xo[k];
+#pragma unroll
+        for (int i = 0; i < RC; ++i) acc[i] += v[i * c + k] * xk;
       }
     }
   }
 }
 
+template <int RC>
 __global__ void __launch_bounds__(kTB) k_spmv_gen(SpmvDev S0, SpmvDev S1, int has1, BlocksDev B,
-                                                  const double* __restrict__ x, double* __restrict__ y, int accumulate,
-                                                  PcgState* st, double* part) {
+                                                  const int32_t* __restrict__ rows, int64_t nrows,
+                                                  const double* __restrict__ x, double* __restrict__ y,
+                                                  int accumulate, const PcgState* st) {
   if (st && st->status) return;
-  double dot[1] = {0.0};
-  for (int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; R < B.nb; R += int64_t(gridDim.x) * blockDim.x) {
-    double acc[16];
-    const int rc = B.rc[R];
-    for (int i = 0; i < rc; ++i) acc[i] = 0.0;
-    acc_gen(S0, R, x, acc);
-    if (has1) acc_gen(S1, R, x, acc);
-    double* yo = y + B.start[R];
-    for (int i = 0; i < rc; ++i) {
-      const double v = accumulate ? yo[i] + acc[i] : acc[i];
-      yo[i] = v;
-      dot[0] += x[B.start[R] + i] * v;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = w0; q < nrows; q += nw) {
+    const int64_t R = rows ? rows[q] : q;
+    double acc[RC];
+#pragma unroll
+    for (int i = 0; i < RC; ++i) acc[i] = 0.0;
+    acc_gen<RC>(S0, R, lane, x, acc);
+    if (has1) acc_gen<RC>(S1, R, lane, x, acc);
+#pragma unroll
+    for (int i = 0; i < RC; ++i)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+    if (lane == 0) {
+      double* yo = y + B.start[R];
+#pragma unroll
+      for (int i = 0; i < RC; ++i) yo[i] = accumulate ? yo[i] + acc[i] : acc[i];
     }
   }
-  if (!part) return;
+}
+
+// pHp over all rows, last CTA -> alpha / status (generic path).
+__global__ void __launch_bounds__(kTB) k_dot_alpha(int64_t s, const double* __restrict__ p,
+                                                   const double* __restrict__ hp, PcgState* st, double* part) {
+  if (st->status) return;
+  double dot[1] = {0.0};
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s; i += int64_t(gridDim.x) * blockDim.x)
+    dot[0] += p[i] * hp[i];
   block_reduce<1>(dot);
   if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
   if (!last_cta(&st->counter1)) return;
@@ -406,12 +433,48 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
   const bool fast = c.uniform3 && s0.all33 && (!has1 || s1->all33);
   SpmvDev d0 = spmv_dev(s0);
   SpmvDev d1 = has1 ? spmv_dev(*s1) : d0;
-  if (fast)
-    k_spmv33<<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
-  else
-    k_spmv_gen<<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, blocks_view(c), x, y, accumulate ? 1 : 0, st,
-                                           part);
-  YS_LAUNCH_CHECK();
+  if (fast) {
+    static const int sw = [] {
+      const char* e = getenv("YS_SPMV_SW");
+      return e ? atoi(e) : 8;
+    }();
+    switch (sw) {
+      case 4: k_spmv33<4><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
+      case 16: k_spmv33<16><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
+      default: k_spmv33<8><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
+    }
+    YS_LAUNCH_CHECK();
+    return;
+  }
+  const BlocksDev B = blocks_view(c);
+  for (size_t k = 0; k < c.rc_classes.size(); ++k) {
+    const int rc = c.rc_classes[k];
+    const int32_t* rows = c.rc_classes.size() == 1 ? nullptr : c.rc_lists[k].p;
+    const int64_t nrows = c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[k].n);
+    if (nrows == 0) continue;
+    const int g = int(std::min<int64_t>(grid, ceil_div(nrows * 32, kTB)));
+#define YS_GEN(RC)                                                                                         \
+  case RC:                                                                                                 \
+    k_spmv_gen<RC><<<g, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, B, rows, nrows, x, y, accumulate ? 1 : 0, st); \
+    break;
+    switch (rc) {
+      YS_GEN(1)
+      YS_GEN(2)
+      YS_GEN(3)
+      YS_GEN(4)
+      YS_GEN(6)
+      YS_GEN(9)
+      YS_GEN(12)
+      default:
+        fail(YS_ERR_INTERNAL, "unsupported block size in SpMV");
+    }
+#undef YS_GEN
+    YS_LAUNCH_CHECK();
+  }
+  if (part) {
+    k_dot_alpha<<<grid, kTB, 0, c.stream>>>(c.s, x, y, st, part);
+    YS_LAUNCH_CHECK();
+  }
 }
 
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y) {
@@ -519,29 +582,46 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
   Structure& s0 = c.S[0];
   Structure& s1 = c.S[1];
   auto P = [](const void* q) { return uint64_t(uintptr_t(q)); };
-  std::vector<uint64_t> key = {P(s0.sp_rowptr.p), P(s0.sp_ent.p), P(s0.values.p), P(s0.row.p), P(s0.col.p),
+  std::vector<uint64_t> key = {P(s0.sp_rowptr.p), P(s0.sp_ent.p), P(s0.values.p), P(s0.sp_oth.p), P(s0.nrow.p), P(s0.trow.p), P(s0.tlist.p), P(s0.col.p),
                                P(s0.br.p), P(s0.bc.p), P(s0.voff.p), P(s1.sp_rowptr.p), P(s1.sp_ent.p),
-                               P(s1.values.p), P(s1.row.p), P(s1.col.p), P(s1.br.p), P(s1.bc.p), P(s1.voff.p),
+                               P(s1.values.p), P(s1.sp_oth.p), P(s1.nrow.p), P(s1.trow.p), P(s1.tlist.p), P(s1.col.p), P(s1.br.p), P(s1.bc.p), P(s1.voff.p),
                                P(c.DX.p), P(c.r.p), P(c.z.p), P(c.p.p), P(c.hp.p), P(c.minv.p), P(c.pcg.p),
                                P(c.partials.p), P(c.hist.p),
                                uint64_t(s1.n_blocks > 0) | (uint64_t(s0.all33) << 1) | (uint64_t(s1.all33) << 2),
                                uint64_t(grid), uint64_t(c.s)};
-  if (!c.pcg_exec || c.pcg_key != key) {
-    drop_pcg_graph(c);
-    if (!build_conditional_graph(c, grid)) build_chunk_graph(c, grid, 8);
-    c.pcg_key = key;
-  }
+  // YS_PCG_GRAPH: "cond" (default: device-side while loop), "chunk" (graph of 8
+  // iterations, host checks the status per chunk), "none" (plain launches —
+  // for ncu, which cannot profile kernels inside conditional graphs).
+  static const int mode = [] {
+    const char* e = getenv("YS_PCG_GRAPH");
+    if (!e) return 0;
+    return std::string(e) == "chunk" ? 1 : std::string(e) == "none" ? 2 : 0;
+  }();
   PcgState fin{};
-  if (c.pcg_cond) {
-    YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
-    YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-    YS_CUDA(cudaStreamSynchronize(s));
-  } else {
+  if (mode == 2) {
     for (;;) {
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
       if (fin.status) break;
+      for (int k = 0; k < 8; ++k) launch_iteration(c, grid, cudaGraphConditionalHandle{}, false);
+    }
+  } else {
+    if (!c.pcg_exec || c.pcg_key != key) {
+      drop_pcg_graph(c);
+      if (mode == 1 || !build_conditional_graph(c, grid)) build_chunk_graph(c, grid, 8);
+      c.pcg_key = key;
+    }
+    if (c.pcg_cond) {
       YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+      YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      YS_CUDA(cudaStreamSynchronize(s));
+    } else {
+      for (;;) {
+        YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        YS_CUDA(cudaStreamSynchronize(s));
+        if (fin.status) break;
+        YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+      }
     }
   }
   c.launches += 2 + 3 * fin.it;

@@ -171,6 +171,13 @@ class Engine:
         self._c(self.f["pair_count"](self.ctx, pairset, C.byref(n)))
         return n.value
 
+    def get_pairs(self, pairset: int) -> np.ndarray:
+        n = self.pair_count(pairset)
+        out = np.zeros(2 * n, dtype=np.int64)
+        if n:
+            self._c(self.f["get_pairs"](self.ctx, pairset, _ip64(out)))
+        return out.reshape(n, 2)
+
     def refresh_pairs(self, pairset: int, dhat: float, child_is_fixed=None) -> int:
         n = C.c_int64()
         if child_is_fixed is None:

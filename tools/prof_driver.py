@@ -1,0 +1,13 @@
+"""Builds a scene's prepared state and runs the hot kernels a few times
+(target command for ncu captures)."""
+import sys
+
+from bench import prepare
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+sim = prepare(name, True, "gpu")
+eng = sim.eng
+st = eng.minimize_step(sim.config.pcg_tol, -1, want_dx=False)
+print("pcg iterations", st.pcg_iterations, flush=True)
+for which in (0, 1, 2):
+    print(which, eng.time_kernel(which, 3), flush=True)
