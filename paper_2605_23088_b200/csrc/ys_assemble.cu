@@ -118,42 +118,75 @@ __device__ __forceinline__ void load_stencil(const EnergyDev& E, const double* _
   }
 }
 
-__global__ void __launch_bounds__(128) k_eval_snh(EnergyDev E, const double* __restrict__ X, int project,
-                                                  int want_h, double* __restrict__ hc, double* __restrict__ gc) {
+// Pass A of the 9x9-projected stencil terms (SNH: KIND 0, bending: KIND 1):
+// gradient, edge-space Hessian, and — when the projection matrix M is positive
+// definite (Cholesky succeeds) — the vertex blocks of M directly.  Indefinite
+// elements are compacted into (list, M) for pass B.
+template <int KIND>
+__global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const double* __restrict__ X, int project,
+                                                        int want_h, double* __restrict__ hc,
+                                                        double* __restrict__ gc, int* err,
+                                                        unsigned int* __restrict__ count,
+                                                        int32_t* __restrict__ list, double* __restrict__ mbuf) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= E.n) return;
   double x[12];
   int32_t gs[4];
   load_stencil(E, X, i, x, gs);
-  double binv[9];
-  const double* cd = E.cdata + 10 * i;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) binv[k] = cd[k];
-  const double vol = cd[9];
-  const SnhParams P{E.prm[0], E.prm[1], E.prm[2], E.prm[3]};
   double g[12];
-  VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
-  snh_local(x, binv, vol, P, want_h != 0, project != 0, E.mode == YS_PROJECT_REDUCED, g, wr);
+  double hd[45];
+  if (KIND == 0) {
+    double binv[9];
+    const double* cd = E.cdata + 10 * i;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) binv[k] = cd[k];
+    const SnhParams P{E.prm[0], E.prm[1], E.prm[2], E.prm[3]};
+    snh_local(x, binv, cd[9], P, want_h != 0, g, hd);
+  } else {
+    if (bending_local(x, E.cdata[i], want_h != 0, g, hd)) atomicOr(err, kErrDiv);
+  }
   double* go = gc + inst_goff(E, i);
 #pragma unroll
   for (int k = 0; k < 12; ++k) go[k] = g[k];
+  if (!want_h) return;
+  const VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
+  if (!project) {
+    expand_vertex_blocks(hd, false, wr);
+    return;
+  }
+  const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
+  if (full) edge_to_projection_space(hd);
+  expand_vertex_blocks(hd, full, wr);  // exact when M is PD; pass B overwrites otherwise
+  if (!cholesky_pd9(hd)) {
+    const unsigned k = atomicAdd(count, 1u);
+    list[k] = int32_t(i);
+    double* m = mbuf + 45 * int64_t(k);
+#pragma unroll
+    for (int q = 0; q < 45; ++q) m[q] = hd[q];
+  }
 }
 
-__global__ void __launch_bounds__(128) k_eval_bending(EnergyDev E, const double* __restrict__ X, int project,
-                                                      int want_h, double* __restrict__ hc,
-                                                      double* __restrict__ gc, int* err) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= E.n) return;
-  double x[12];
-  int32_t gs[4];
-  load_stencil(E, X, i, x, gs);
-  double g[12];
-  VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
-  const int st = bending_local(x, E.cdata[i], want_h != 0, project != 0, g, wr);
-  if (st) atomicOr(err, kErrDiv);
-  double* go = gc + inst_goff(E, i);
+// Pass B: Jacobi EVD + clamp + reconstruction for the compacted indefinite
+// elements only (fully populated warps), then the vertex blocks.
+template <int KIND>
+__global__ void __launch_bounds__(128) k_eval_stencil_b(EnergyDev E, double* __restrict__ hc,
+                                                        const unsigned int* __restrict__ count,
+                                                        const int32_t* __restrict__ list,
+                                                        const double* __restrict__ mbuf) {
+  const unsigned n = *count;
+  const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int64_t i = list[k];
+    double m[45];
+    const double* src = mbuf + 45 * int64_t(k);
 #pragma unroll
-  for (int k = 0; k < 12; ++k) go[k] = g[k];
+    for (int q = 0; q < 45; ++q) m[q] = src[q];
+    psd_project9(m);
+    const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
+    const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
+    const VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
+    expand_vertex_blocks(m, full, wr);
+  }
 }
 
 __global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* __restrict__ X, int project,
@@ -614,6 +647,8 @@ static void record(Context& c, int idx) {
 
 void ctx_eval_all(Context& c, bool project, bool with_hessian) {
   cudaStream_t s = c.stream;
+  c.evd_count.resize(std::max(c.evd_count.n, c.energies.size()));
+  c.evd_count.zero(s);
   for (size_t id = 0; id < c.energies.size(); ++id) {
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
@@ -622,12 +657,23 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
     const int proj = project ? 1 : 0, wh = with_hessian ? 1 : 0;
     switch (e.kind) {
       case K_SNH:
-        k_eval_snh<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
+      case K_BENDING: {
+        c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * e.n)));
+        c.evd_list.resize(std::max(c.evd_list.n, size_t(e.n)));
+        unsigned int* cnt = c.evd_count.p + id;
+        const unsigned ga = grid_for(e.n, 128), gb = unsigned(sm_count() * 4);
+        if (e.kind == K_SNH) {
+          k_eval_stencil_a<0><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
+                                                 c.evd_list.p, c.evd_m.p);
+          if (wh && proj) k_eval_stencil_b<0><<<gb, 128, 0, s>>>(E, st.hcontrib.p, cnt, c.evd_list.p, c.evd_m.p);
+        } else {
+          k_eval_stencil_a<1><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
+                                                 c.evd_list.p, c.evd_m.p);
+          if (wh && proj) k_eval_stencil_b<1><<<gb, 128, 0, s>>>(E, st.hcontrib.p, cnt, c.evd_list.p, c.evd_m.p);
+        }
+        ++c.launches;
         break;
-      case K_BENDING:
-        k_eval_bending<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
-                                                          c.errflag.p);
-        break;
+      }
       case K_ORTHO:
         k_eval_ortho<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
         break;

@@ -816,8 +816,8 @@ int ys_energy_totals(ys_context* c, double* t) {
 int ys_apply_hessian(ys_context* c, const double* x, double* y) {
   return guarded(c, [&] {
     require_finalized(*c);
-    c->r.resize(c->s);
-    c->hp.resize(c->s);
+    c->r.resize(c->s + 2);
+    c->hp.resize(c->s + 2);
     YS_CUDA(cudaMemcpyAsync(c->r.p, x, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     YS_CUDA(cudaMemcpyAsync(c->hp.p, y, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     ctx_apply_hessian_dev(*c, c->r.p, c->hp.p);
@@ -1003,7 +1003,15 @@ int ys_set_profiling(ys_context* c, int32_t on) {
 int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
   return guarded(c, [&] {
     for (int k = 0; k < 7; ++k) ms[k] = c->stage_ms[k];
-    if (counts) counts[0] = c->launches;
+    if (counts) {
+      counts[0] = c->launches;
+      int64_t evd = 0;
+      if (c->evd_count.n) {
+        std::vector<unsigned int> h = c->evd_count.to_host(c->stream);
+        for (unsigned v : h) evd += v;
+      }
+      counts[1] = evd;  // indefinite 9x9 projections (EVD pass) in the last assembly
+    }
   });
 }
 
@@ -1093,8 +1101,8 @@ int ys_bsr_set_values(ys_context* c, int32_t id, const double* v) {
 int ys_bsr_spmv(ys_context* c, int32_t id, const double* x, double* y) {
   return guarded(c, [&] {
     ys_context& b = bsr_of(c, id);
-    b.r.resize(b.s);
-    b.hp.resize(b.s);
+    b.r.resize(b.s + 2);
+    b.hp.resize(b.s + 2);
     YS_CUDA(cudaMemcpyAsync(b.r.p, x, b.s * sizeof(double), cudaMemcpyHostToDevice, b.stream));
     YS_CUDA(cudaMemcpyAsync(b.hp.p, y, b.s * sizeof(double), cudaMemcpyHostToDevice, b.stream));
     spmv_launch(b, b.S[0], nullptr, b.r.p, b.hp.p, true, nullptr, nullptr, pcg_grid(b));
@@ -1152,8 +1160,8 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
       }
     };
     if (which == 0) {
-      c->p.resize(c->s);
-      c->hp.resize(c->s);
+      c->p.resize(c->s + 2);
+      c->hp.resize(c->s + 2);
       YS_CUDA(cudaMemcpyAsync(c->p.p, c->G.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, s));
       // 8 r c (values) + 8 (two int32 coords) per upper block, 16 s per SpMV
       for (int w = 0; w < 2; ++w)

@@ -192,6 +192,12 @@ struct Context {
   std::vector<int32_t> rc_classes;   // distinct target block sizes
   std::vector<DevBuf<int32_t>> rc_lists;  // block ids per rc class (non-uniform layouts)
 
+  // two-pass projection of 9x9 edge-space Hessians (SNH, bending)
+  DevBuf<double> evd_m;          // pending M (45 per entry)
+  DevBuf<int32_t> evd_list;      // pending element ids
+  DevBuf<unsigned int> evd_count;  // one counter per energy
+  int64_t evd_last = 0;          // indefinite elements of the last assembly (diagnostics)
+
   // profiling
   bool profiling = false;
   double stage_ms[8] = {0};

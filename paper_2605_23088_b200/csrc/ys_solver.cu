@@ -105,32 +105,84 @@ __device__ __forceinline__ void sum_partials(const double* part, int n, int stri
 // contiguous u range [nrow[R], nrow[R+1]) (y_R += B x_c); the blocks (r, R),
 // r < R, come from tlist (y_R += B^T x_r) and are mostly L2 hits — row r
 // streamed them moments earlier.
+// 16-byte-aligned window loads: a 3x3 block (72 B at 8-byte alignment) is
+// read as five 16 B loads of the enclosing 80 B window, a 3-vector (24 B) as
+// two 16 B loads — fewer L1 wavefronts than nine / three 8 B loads.  The
+// buffers carry 16 B of tail padding so the windows never leave the allocation.
+__device__ __forceinline__ void load_block9(const double* __restrict__ p, double (&v)[9]) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
+  const double2 w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3), w4 = __ldg(w + 4);
+  if (a & 8) {
+    v[0] = w0.y; v[1] = w1.x; v[2] = w1.y; v[3] = w2.x; v[4] = w2.y;
+    v[5] = w3.x; v[6] = w3.y; v[7] = w4.x; v[8] = w4.y;
+  } else {
+    v[0] = w0.x; v[1] = w0.y; v[2] = w1.x; v[3] = w1.y; v[4] = w2.x;
+    v[5] = w2.y; v[6] = w3.x; v[7] = w3.y; v[8] = w4.x;
+  }
+}
+
+__device__ __forceinline__ void load_vec3(const double* __restrict__ p, double& x0, double& x1, double& x2) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
+  const double2 w0 = w[0], w1 = w[1];
+  if (a & 8) {
+    x0 = w0.y; x1 = w1.x; x2 = w1.y;
+  } else {
+    x0 = w0.x; x1 = w0.y; x2 = w1.x;
+  }
+}
+
+// Block row R of a 3x3 upper-storage structure: its own blocks (R, c) are the
+// contiguous u range [nrow[R], nrow[R+1]) (y_R += B x_c); the blocks (r, R),
+// r < R, come from tlist (y_R += B^T x_r) and are mostly L2 hits — row r
+// streamed them moments earlier.  Both kinds share one slot loop (a
+// transposed block is transposed in registers), so a lane's loads for its
+// slots are independent and issue together.
+struct RowPtrs {
+  int32_t n0, n1, t0, t1;
+};
+
+__device__ __forceinline__ RowPtrs load_rowptrs(const SpmvDev& S, int64_t R) {
+  return RowPtrs{S.nrow[R], S.nrow[R + 1], S.trow[R], S.trow[R + 1]};
+}
+
 template <int SW>
-__device__ __forceinline__ void acc33(const SpmvDev& S, int64_t R, int lane, const double* __restrict__ x, double& a0,
-                                      double& a1, double& a2) {
-  const int32_t n0 = S.nrow[R], n1 = S.nrow[R + 1];
-  const int32_t t0 = S.trow[R], t1 = S.trow[R + 1];
-  for (int32_t u = n0 + lane; u < n1; u += SW) {
-    const double* __restrict__ v = S.values + 9 * int64_t(u);
-    const double* __restrict__ xo = x + S.col[u];
-    const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
+__device__ __forceinline__ void acc33(const SpmvDev& S, const RowPtrs& rp, int lane, const double* __restrict__ x,
+                                      double& a0, double& a1, double& a2) {
+  const int32_t nn = rp.n1 - rp.n0;
+  const int32_t tot = nn + (rp.t1 - rp.t0);
+#pragma unroll 2
+  for (int32_t k = lane; k < tot; k += SW) {
+    const bool tr = k >= nn;
+    int32_t u, o;
+    if (tr) {
+      const int2 t = S.tlist[rp.t0 + (k - nn)];
+      u = t.x;
+      o = t.y;
+    } else {
+      u = rp.n0 + k;
+      o = S.col[u];
+    }
+    double v[9];
+    load_block9(S.values + 9 * int64_t(u), v);
+    double x0, x1, x2;
+    load_vec3(x + o, x0, x1, x2);
+    if (tr) {  // B^T
+      double t;
+      t = v[1]; v[1] = v[3]; v[3] = t;
+      t = v[2]; v[2] = v[6]; v[6] = t;
+      t = v[5]; v[5] = v[7]; v[7] = t;
+    }
     a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
     a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
     a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
   }
-  for (int32_t j = t0 + lane; j < t1; j += SW) {
-    const int2 t = S.tlist[j];
-    const double* __restrict__ v = S.values + 9 * int64_t(t.x);
-    const double* __restrict__ xo = x + t.y;
-    const double x0 = xo[0], x1 = xo[1], x2 = xo[2];
-    a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
-    a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
-    a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
-  }
 }
 
 // y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials
-// reduced to pHp and alpha by the last CTA.
+// reduced to pHp and alpha by the last CTA.  The grid is one resident wave
+// (occupancy-sized) and each sub-warp prefetches its next row's pointers.
 template <int SW>
 __global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
                                                 const double* __restrict__ x, double* __restrict__ y, int accumulate,
@@ -141,10 +193,20 @@ __global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1
   const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
   const unsigned mask = (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u)) << ((threadIdx.x & 31) & ~(SW - 1));
   double dot[1] = {0.0};
+  RowPtrs p0{}, p1{};
+  if (sw0 < nb) {
+    p0 = load_rowptrs(S0, sw0);
+    if (has1) p1 = load_rowptrs(S1, sw0);
+  }
   for (int64_t R = sw0; R < nb; R += nsw) {
+    const RowPtrs c0 = p0, c1 = p1;
+    if (R + nsw < nb) {  // prefetch the next row's pointers
+      p0 = load_rowptrs(S0, R + nsw);
+      if (has1) p1 = load_rowptrs(S1, R + nsw);
+    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33<SW>(S0, R, lane, x, a0, a1, a2);
-    if (has1) acc33<SW>(S1, R, lane, x, a0, a1, a2);
+    acc33<SW>(S0, c0, lane, x, a0, a1, a2);
+    if (has1) acc33<SW>(S1, c1, lane, x, a0, a1, a2);
 #pragma unroll
     for (int off = SW / 2; off > 0; off >>= 1) {
       a0 += __shfl_xor_sync(mask, a0, off, SW);
@@ -438,10 +500,19 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
       const char* e = getenv("YS_SPMV_SW");
       return e ? atoi(e) : 8;
     }();
+    static int occ[3] = {0, 0, 0};
+    auto waves = [&](auto kern, int idx) {
+      if (!occ[idx]) {
+        YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[idx], kern, kTB, 0));
+        if (occ[idx] < 1) occ[idx] = 1;
+      }
+      // one resident wave, never more CTAs than the partial buffer holds
+      return std::min(grid, occ[idx] * sm_count());
+    };
     switch (sw) {
-      case 4: k_spmv33<4><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
-      case 16: k_spmv33<16><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
-      default: k_spmv33<8><<<grid, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
+      case 4: k_spmv33<4><<<waves(k_spmv33<4>, 0), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
+      case 16: k_spmv33<16><<<waves(k_spmv33<16>, 2), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
+      default: k_spmv33<8><<<waves(k_spmv33<8>, 1), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
     }
     YS_LAUNCH_CHECK();
     return;
@@ -559,10 +630,10 @@ int pcg_grid(Context& c) { return std::max(1, sm_count() * 8); }
 void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev, ys_step_stats* stats) {
   cudaStream_t s = c.stream;
   const int grid = pcg_grid(c);
-  c.r.resize(c.s);
-  c.z.resize(c.s);
-  c.p.resize(c.s);
-  c.hp.resize(c.s);
+  c.r.resize(c.s + 2);
+  c.z.resize(c.s + 2);
+  c.p.resize(c.s + 2);
+  c.hp.resize(c.s + 2);
   c.pcg.resize(1);
   c.partials.resize(std::max<size_t>(c.partials.n, size_t(2 * grid)));
   const int64_t hist_cap = std::min<int64_t>(max_iter, int64_t(1) << 22) + 2;

@@ -389,7 +389,8 @@ void build_structure_from_keys(Context& c, Structure& st, DevBuf<uint64_t>& keys
   }
   st.n_blocks = hsum->nu;
   st.n_values = hsum->n_values;
-  st.values.resize(size_t(st.n_values));
+  st.values.resize(size_t(st.n_values) + 2);  // +16 B: aligned-window loads of the last block
+  st.values.n = size_t(st.n_values);
 }
 
 void build_spmv_plan(Context& c, Structure& st, const BlocksDev& blocks) {

@@ -137,40 +137,37 @@ __device__ __forceinline__ int psd_project9(double* a) {
 // ---------------------------------------------------------------------------
 // Edge-space (9x9, index 3*edge + coord) Hessian H_D -> vertex blocks.
 //
-// project && !reduced : M = (R (x) I) H_D (R^T (x) I); Proj9(M); E = W
-// project &&  reduced : Proj9(H_D); E = S^T           (ReducedProject)
-// !project            : E = S^T, no projection         (assemble(false))
-// Output: for each vertex pair (a, b), a <= b in slot order, the 3x3 block
-// H_x[a][b] (row coords of a, col coords of b) handed to wr(pair, k, kk, v),
-// pair order (0,0),(0,1),(0,2),(0,3),(1,1),(1,2),(1,3),(2,2),(2,3),(3,3).
+// FullProject:    M = (R (x) I) H_D (R^T (x) I), P = Proj9(M), E = W
+// ReducedProject: M = H_D, P = Proj9(M), E = S^T
+// no projection:  P = H_D, E = S^T                   (assemble(false))
+// Vertex block (a, b) = sum_{i,i'} E[a][i] E[b][i'] P_{ii'}; pair order
+// (0,0),(0,1),(0,2),(0,3),(1,1),(1,2),(1,3),(2,2),(2,3),(3,3).
+
+// In place: hd <- (R (x) I) hd (R^T (x) I)   (blocks, HD_{ii'} = HD_{i'i}^T)
+__device__ __forceinline__ void edge_to_projection_space(double* hd) {
+  double m[45];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = a; b < 3; ++b)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          if (a == b && kk < k) continue;
+          double acc = 0.0;
+#pragma unroll
+          for (int i = a; i < 3; ++i)
+#pragma unroll
+            for (int ip = b; ip < 3; ++ip) acc += kR(a, i) * kR(b, ip) * hd[pk9(3 * i + k, 3 * ip + kk)];
+          m[pk9(3 * a + k, 3 * b + kk)] = acc;
+        }
+#pragma unroll
+  for (int i = 0; i < 45; ++i) hd[i] = m[i];
+}
+
 template <class Writer>
-__device__ __forceinline__ void edge_hessian_to_vertex_blocks(double* hd, bool project, bool reduced,
-                                                              const Writer& wr) {
-  const bool full = project && !reduced;
-  if (full) {
-    // M_ab = sum_{i>=a, i'>=b} R[a][i] R[b][i'] HD_{ii'}  (blocks, HD_{ii'} = HD_{i'i}^T)
-    double m[45];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = a; b < 3; ++b)
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-          for (int kk = 0; kk < 3; ++kk) {
-            if (a == b && kk < k) continue;
-            double acc = 0.0;
-#pragma unroll
-            for (int i = a; i < 3; ++i)
-#pragma unroll
-              for (int ip = b; ip < 3; ++ip) acc += kR(a, i) * kR(b, ip) * hd[pk9(3 * i + k, 3 * ip + kk)];
-            m[pk9(3 * a + k, 3 * b + kk)] = acc;
-          }
-#pragma unroll
-    for (int i = 0; i < 45; ++i) hd[i] = m[i];
-  }
-  if (project) psd_project9(hd);
-  // expansion
+__device__ __forceinline__ void expand_vertex_blocks(const double* hd, bool full, const Writer& wr) {
 #pragma unroll
   for (int a = 0, pair = 0; a < 4; ++a)
 #pragma unroll
@@ -193,6 +190,33 @@ __device__ __forceinline__ void edge_hessian_to_vertex_blocks(double* hd, bool p
           wr(pair, k, kk, acc);
           if (a == b && kk != k) wr(pair, kk, k, acc);
         }
+}
+
+// Positive-definiteness test by Cholesky on a copy: true iff every pivot is
+// positive, in which case Proj9(M) = M (the reference's clamp is a no-op).
+__device__ __forceinline__ bool cholesky_pd9(const double* m) {
+  double l[45];
+#pragma unroll
+  for (int i = 0; i < 45; ++i) l[i] = m[i];
+  bool pd = true;
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    double d = l[pk9(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) d -= l[pk9(j, k)] * l[pk9(j, k)];
+    pd = pd && (d > 0.0);
+    const double ljj = sqrt(d > 0.0 ? d : 1.0);
+    l[pk9(j, j)] = ljj;
+    const double inv = 1.0 / ljj;
+#pragma unroll
+    for (int i = j + 1; i < 9; ++i) {
+      double v = l[pk9(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v -= l[pk9(i, k)] * l[pk9(j, k)];
+      l[pk9(i, j)] = v * inv;
+    }
+  }
+  return pd;
 }
 
 // ---------------------------------------------------------------------------
@@ -251,10 +275,9 @@ __device__ __forceinline__ bool snh_energy(const double x[12], const double binv
 }
 
 // Gradient (12, vertex-major) and vertex blocks of the (projected) Hessian.
-template <class Writer>
+// Gradient (12, vertex-major) and, if want_h, the edge-space Hessian H_D (packed 45).
 __device__ __forceinline__ void snh_local(const double x[12], const double binv[9], double vol,
-                                          const SnhParams& P, bool want_h, bool project, bool reduced,
-                                          double g[12], const Writer& blk) {
+                                          const SnhParams& P, bool want_h, double g[12], double* hd) {
   double fi[9];
   snh_fi(x, binv, fi);
   double ic = 0.0;
@@ -291,7 +314,6 @@ __device__ __forceinline__ void snh_local(const double x[12], const double binv[
   const double c2 = vw * 2.0 * P.mu * ip1 * ip1;
   const double c3 = vw * P.lambda;
   // H_D blocks: HD_{ii'} = Binv A_{ii'} Binv^T, computed blockwise into packed hd
-  double hd[45];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -329,7 +351,6 @@ __device__ __forceinline__ void snh_local(const double x[12], const double binv[
               binv[3 * k + 0] * t[0 * 3 + kp] + binv[3 * k + 1] * t[1 * 3 + kp] + binv[3 * k + 2] * t[2 * 3 + kp];
         }
     }
-  edge_hessian_to_vertex_blocks(hd, project, reduced, blk);
 }
 
 // ---------------------------------------------------------------------------
@@ -370,9 +391,7 @@ __device__ __forceinline__ void skew3(const double a[3], double m[9]) {
   m[6] = -a[1]; m[7] = a[0];  m[8] = 0.0;
 }
 
-template <class Writer>
-__device__ __forceinline__ int bending_local(const double x[12], double c, bool want_h, bool project,
-                                             double g[12], const Writer& blk) {
+__device__ __forceinline__ int bending_local(const double x[12], double c, bool want_h, double g[12], double* hd) {
   double e0[3], e1[3], e2[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -465,7 +484,6 @@ __device__ __forceinline__ int bending_local(const double x[12], double c, bool 
       z2[3 * a + b] = (3.0 * d2 * h2[a] * h2[b] - uh[a] * h2[b] - h2[a] * uh[b] - (a == b ? d2 : 0.0)) / (N2 * N2);
     }
   // q = (I - u^ u^^T)/U
-  double hd[45];
 #pragma unroll
   for (int p = 0; p < 9; ++p)
 #pragma unroll
@@ -502,7 +520,6 @@ __device__ __forceinline__ int bending_local(const double x[12], double c, bool 
     }
 #pragma unroll
   for (int i = 0; i < 45; ++i) hd[i] *= c;
-  edge_hessian_to_vertex_blocks(hd, project, false, blk);
   return 0;
 }
 

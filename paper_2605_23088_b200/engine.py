@@ -397,10 +397,12 @@ class Engine:
         self._c(self.f["time_kernel"](self.ctx, which, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
-    def stage_times(self):
+    def stage_times(self, with_counts: bool = False):
         ms = np.zeros(8)
         cnt = np.zeros(2, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
+        if with_counts:
+            return ms, int(cnt[0]), int(cnt[1])
         return ms, int(cnt[0])
 
 
