@@ -67,7 +67,24 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    _build_cpp_smoke()
     return LIB
+
+
+def _build_cpp_smoke():
+    """The C++ facade example (include/yasps_b200.hpp) linked against the library."""
+    src = PKG.parent / "tools" / "cpp_smoke.cpp"
+    out = PKG.parent / "tools" / "cpp_smoke"
+    if not src.exists():
+        return
+    if out.exists() and out.stat().st_mtime > max(src.stat().st_mtime, LIB.stat().st_mtime,
+                                                   (INCLUDE / "yasps_b200.hpp").stat().st_mtime):
+        return
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", str(INCLUDE), str(src), "-L", str(PKG), "-lyasps_b200",
+           "-Wl,-rpath,$ORIGIN/../paper_2605_23088_b200", "-o", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cpp_smoke build failed:\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -99,3 +99,14 @@ def test_config_errors():
 def test_scene_configs_parse(name):
     cfg = SimConfig.from_dict(configs.CONFIGS[name]())
     assert cfg.contact_enabled and len(cfg.bodies) >= 2
+
+
+@pytest.mark.gpu
+def test_cpp_facade_on_device():
+    """C++ host through include/yasps_b200.hpp (tools/cpp_smoke.cpp)."""
+    import subprocess
+    exe = ROOT / "tools" / "cpp_smoke"
+    assert exe.exists(), "built by paper_2605_23088_b200/build.py"
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "cpp facade ok" in r.stdout
