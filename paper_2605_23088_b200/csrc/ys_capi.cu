@@ -51,6 +51,7 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
 void ctx_gather_all(Context& c);
+bool spmv_variant(Context& c, int v, const double* x, double* y);
 
 void ctx_eval_all(Context& c, bool project, bool with_hessian);
 
@@ -1003,6 +1004,7 @@ int ys_set_profiling(ys_context* c, int32_t on) {
 int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
   return guarded(c, [&] {
     for (int k = 0; k < 7; ++k) ms[k] = c->stage_ms[k];
+    for (int k = 0; k < 4; ++k) ms[8 + k] = c->pcg_phase_ms[k];
     if (counts) {
       counts[0] = c->launches;
       int64_t evd = 0;
@@ -1150,7 +1152,9 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
     cudaStream_t s = c->stream;
     double alg = 0.0;
     auto launch = [&]() {
-      if (which == 0) {
+      if (which >= 10) {
+        if (!spmv_variant(*c, which - 10, c->p.p, c->hp.p)) fail(YS_ERR_VALIDATION, "unknown SpMV variant");
+      } else if (which == 0) {
         spmv_launch(*c, c->S[0], &c->S[1], c->p.p, c->hp.p, false, nullptr, nullptr, pcg_grid(*c));
       } else if (which == 1) {
         ctx_gather_all(*c);
@@ -1159,7 +1163,7 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
         ctx_eval_all(*c, true, true);
       }
     };
-    if (which == 0) {
+    if (which == 0 || which >= 10) {
       c->p.resize(c->s + 2);
       c->hp.resize(c->s + 2);
       YS_CUDA(cudaMemcpyAsync(c->p.p, c->G.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, s));

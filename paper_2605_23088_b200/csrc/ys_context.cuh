@@ -132,6 +132,7 @@ struct PcgState {
   int status;  // 0 running, 1 converged, 2 stagnated (pHp == 0), 3 curvature error, 4 residual error, 5 max_iter
   int fail_it;
   unsigned int counter1, counter2;
+  unsigned long long phase_ns[4];  // persistent PCG: SpMV+pHp, reduce+update, reduce, p-update (CTA 0 view)
 };
 
 struct Context {
@@ -169,6 +170,7 @@ struct Context {
   // PCG
   DevBuf<double> r, z, p, hp;
   DevBuf<PcgState> pcg;
+  DevBuf<unsigned char> gridbar;
   DevBuf<double> partials;
   DevBuf<double> hist;
   int64_t hist_count = 0;
@@ -201,6 +203,7 @@ struct Context {
   // profiling
   bool profiling = false;
   double stage_ms[8] = {0};
+  double pcg_phase_ms[4] = {0};
   int64_t launches = 0;
   cudaEvent_t ev[10] = {};
 

@@ -122,6 +122,18 @@ __device__ __forceinline__ void load_block9(const double* __restrict__ p, double
   }
 }
 
+// L2-coherent variant (data written earlier in the same persistent kernel).
+__device__ __forceinline__ void load_vec3_cg(const double* p, double& x0, double& x1, double& x2) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
+  const double2 w0 = __ldcg(w), w1 = __ldcg(w + 1);
+  if (a & 8) {
+    x0 = w0.y; x1 = w1.x; x2 = w1.y;
+  } else {
+    x0 = w0.x; x1 = w0.y; x2 = w1.x;
+  }
+}
+
 __device__ __forceinline__ void load_vec3(const double* __restrict__ p, double& x0, double& x1, double& x2) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
@@ -134,11 +146,11 @@ __device__ __forceinline__ void load_vec3(const double* __restrict__ p, double& 
 }
 
 // Block row R of a 3x3 upper-storage structure: its own blocks (R, c) are the
-// contiguous u range [nrow[R], nrow[R+1]) (y_R += B x_c); the blocks (r, R),
-// r < R, come from tlist (y_R += B^T x_r) and are mostly L2 hits — row r
-// streamed them moments earlier.  Both kinds share one slot loop (a
-// transposed block is transposed in registers), so a lane's loads for its
-// slots are independent and issue together.
+// contiguous u range [nrow[R], nrow[R+1]) (y_R += B x_c, no index); the blocks
+// (r, R), r < R, come from tlist (y_R += B^T x_r) and are mostly L2 hits — row
+// r streamed them moments earlier.  The kernel is latency-bound on these
+// dependent gathers, so it is shaped for rows in flight: 4 lanes per row,
+// <= 64 registers (4 CTAs of 256 per SM), one resident wave.
 struct RowPtrs {
   int32_t n0, n1, t0, t1;
 };
@@ -150,63 +162,49 @@ __device__ __forceinline__ RowPtrs load_rowptrs(const SpmvDev& S, int64_t R) {
 template <int SW>
 __device__ __forceinline__ void acc33(const SpmvDev& S, const RowPtrs& rp, int lane, const double* __restrict__ x,
                                       double& a0, double& a1, double& a2) {
-  const int32_t nn = rp.n1 - rp.n0;
-  const int32_t tot = nn + (rp.t1 - rp.t0);
-#pragma unroll 2
-  for (int32_t k = lane; k < tot; k += SW) {
-    const bool tr = k >= nn;
-    int32_t u, o;
-    if (tr) {
-      const int2 t = S.tlist[rp.t0 + (k - nn)];
-      u = t.x;
-      o = t.y;
-    } else {
-      u = rp.n0 + k;
-      o = S.col[u];
-    }
+  for (int32_t u = rp.n0 + lane; u < rp.n1; u += SW) {
     double v[9];
     load_block9(S.values + 9 * int64_t(u), v);
     double x0, x1, x2;
-    load_vec3(x + o, x0, x1, x2);
-    if (tr) {  // B^T
-      double t;
-      t = v[1]; v[1] = v[3]; v[3] = t;
-      t = v[2]; v[2] = v[6]; v[6] = t;
-      t = v[5]; v[5] = v[7]; v[7] = t;
-    }
+    load_vec3(x + S.col[u], x0, x1, x2);
     a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
     a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
     a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
   }
+  for (int32_t j = rp.t0 + lane; j < rp.t1; j += SW) {
+    const int2 t = S.tlist[j];
+    double v[9];
+    load_block9(S.values + 9 * int64_t(t.x), v);
+    double x0, x1, x2;
+    load_vec3(x + t.y, x0, x1, x2);
+    a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
+    a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
+    a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
+  }
 }
 
+constexpr int kSpmvSW = 4;
+
 // y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials
-// reduced to pHp and alpha by the last CTA.  The grid is one resident wave
-// (occupancy-sized) and each sub-warp prefetches its next row's pointers.
-template <int SW>
-__global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
-                                                const double* __restrict__ x, double* __restrict__ y, int accumulate,
-                                                PcgState* st, double* part) {
+// reduced to pHp and alpha by the last CTA.
+__global__ void __launch_bounds__(kTB, 4) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   int accumulate, PcgState* st, double* part) {
+  constexpr int SW = kSpmvSW;
   if (st && st->status) return;
   const int lane = threadIdx.x % SW;
   const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
   const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
-  const unsigned mask = (SW == 32 ? 0xffffffffu : ((1u << SW) - 1u)) << ((threadIdx.x & 31) & ~(SW - 1));
+  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
   double dot[1] = {0.0};
-  RowPtrs p0{}, p1{};
-  if (sw0 < nb) {
-    p0 = load_rowptrs(S0, sw0);
-    if (has1) p1 = load_rowptrs(S1, sw0);
-  }
   for (int64_t R = sw0; R < nb; R += nsw) {
-    const RowPtrs c0 = p0, c1 = p1;
-    if (R + nsw < nb) {  // prefetch the next row's pointers
-      p0 = load_rowptrs(S0, R + nsw);
-      if (has1) p1 = load_rowptrs(S1, R + nsw);
-    }
+    // both groups' row pointers issue together (one latency round, not two)
+    const RowPtrs p0 = load_rowptrs(S0, R);
+    RowPtrs p1{0, 0, 0, 0};
+    if (has1) p1 = load_rowptrs(S1, R);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33<SW>(S0, c0, lane, x, a0, a1, a2);
-    if (has1) acc33<SW>(S1, c1, lane, x, a0, a1, a2);
+    acc33<SW>(S0, p0, lane, x, a0, a1, a2);
+    if (has1) acc33<SW>(S1, p1, lane, x, a0, a1, a2);
 #pragma unroll
     for (int off = SW / 2; off > 0; off >>= 1) {
       a0 += __shfl_xor_sync(mask, a0, off, SW);
@@ -247,6 +245,88 @@ __global__ void __launch_bounds__(kTB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1
       st->alpha = st->rz / php;
     }
   }
+}
+
+// Diagnostic variants of the 3x3 SpMV (YS_SPMV_VARIANT): register caps and
+// partial work, used to attribute the kernel's time (not used by PCG).
+template <int SW, int MINB, int PART, bool PREF>
+__global__ void __launch_bounds__(kTB, MINB) k_spmv33_var(SpmvDev S0, int64_t nb, const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+  const int lane = threadIdx.x % SW;
+  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
+  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
+  RowPtrs nxt{};
+  if (PREF && sw0 < nb) nxt = load_rowptrs(S0, sw0);
+  for (int64_t R = sw0; R < nb; R += nsw) {
+    RowPtrs rp;
+    if (PREF) {
+      rp = nxt;
+      if (R + nsw < nb) nxt = load_rowptrs(S0, R + nsw);
+    } else {
+      rp = load_rowptrs(S0, R);
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    if (PART != 2)
+      for (int32_t u = rp.n0 + lane; u < rp.n1; u += SW) {
+        double v[9];
+        load_block9(S0.values + 9 * int64_t(u), v);
+        double x0 = 1.0, x1 = 1.0, x2 = 1.0;
+        if (PART != 3) load_vec3(x + S0.col[u], x0, x1, x2);
+        a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
+        a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
+        a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
+      }
+    if (PART != 1)
+      for (int32_t j = rp.t0 + lane; j < rp.t1; j += SW) {
+        const int2 t = S0.tlist[j];
+        double v[9];
+        load_block9(S0.values + 9 * int64_t(t.x), v);
+        double x0 = 1.0, x1 = 1.0, x2 = 1.0;
+        if (PART != 3) load_vec3(x + t.y, x0, x1, x2);
+        a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
+        a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
+        a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
+      }
+#pragma unroll
+    for (int off = SW / 2; off > 0; off >>= 1) {
+      a0 += __shfl_xor_sync(mask, a0, off, SW);
+      a1 += __shfl_xor_sync(mask, a1, off, SW);
+      a2 += __shfl_xor_sync(mask, a2, off, SW);
+    }
+    if (lane == 0) {
+      y[3 * R] = a0;
+      y[3 * R + 1] = a1;
+      y[3 * R + 2] = a2;
+    }
+  }
+}
+
+template <class K>
+static void launch_var(Context& c, K kern, SpmvDev d0, const double* x, double* y) {
+  int occ = 0;
+  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+  kern<<<std::max(1, occ) * sm_count(), kTB, 0, c.stream>>>(d0, c.NB, x, y);
+  YS_LAUNCH_CHECK();
+}
+
+bool spmv_variant(Context& c, int v, const double* x, double* y) {
+  SpmvDev d0 = spmv_dev(c.S[0]);
+  switch (v) {
+    case 1: launch_var(c, k_spmv33_var<8, 3, 0, false>, d0, x, y); return true;
+    case 2: launch_var(c, k_spmv33_var<8, 4, 0, false>, d0, x, y); return true;
+    case 3: launch_var(c, k_spmv33_var<8, 5, 0, false>, d0, x, y); return true;
+    case 4: launch_var(c, k_spmv33_var<8, 4, 1, false>, d0, x, y); return true;  // own-row blocks only
+    case 5: launch_var(c, k_spmv33_var<8, 4, 2, false>, d0, x, y); return true;  // transposed only
+    case 6: launch_var(c, k_spmv33_var<8, 4, 3, false>, d0, x, y); return true;  // no x gathers
+    case 7: launch_var(c, k_spmv33_var<8, 4, 0, true>, d0, x, y); return true;   // + row-pointer prefetch
+    case 8: launch_var(c, k_spmv33_var<4, 4, 0, false>, d0, x, y); return true;  // 4 lanes per row
+    case 9: launch_var(c, k_spmv33_var<4, 4, 0, true>, d0, x, y); return true;
+    case 10: launch_var(c, k_spmv33_var<16, 4, 0, false>, d0, x, y); return true;
+    case 11: launch_var(c, k_spmv33_var<4, 5, 0, true>, d0, x, y); return true;
+    case 12: launch_var(c, k_spmv33_var<2, 4, 0, true>, d0, x, y); return true;
+  }
+  return false;
 }
 
 // Generic shapes: one warp per block row of size RC (launched per block-size
@@ -482,8 +562,218 @@ __global__ void k_pupdate(int64_t s, const double* __restrict__ z, double* __res
   if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, status == 0 ? 1u : 0u);
   if (status) return;
   const double b = st->beta;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s; i += int64_t(gridDim.x) * blockDim.x)
-    p[i] = z[i] + b * p[i];
+  // 16-byte vectors (the PCG vectors are 16-byte aligned, s may be odd)
+  const int64_t n2 = s >> 1;
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(gridDim.x) * blockDim.x) {
+    const double2 zz = z2[i];
+    double2 pp = p2[i];
+    pp.x = zz.x + b * pp.x;
+    pp.y = zz.y + b * pp.y;
+    p2[i] = pp;
+  }
+  if ((s & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[s - 1] = z[s - 1] + b * p[s - 1];
+}
+
+// ---------------------------------------------------------------------------
+// Persistent PCG for uniform 3x3 systems: the whole solve is one cooperative
+// launch.  Phases (SpMV + pHp, update + precondition + dots, p update) are
+// separated by a grid barrier; after each barrier every CTA reduces the same
+// per-CTA partials in the same fixed order, so all CTAs hold bit-identical
+// alpha / beta / status without a last-CTA round trip (deterministic).
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBar* gb) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &gb->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(&gb->count, 1u) == gridDim.x - 1) {
+      gb->count = 0;
+      __threadfence();
+      atomicAdd(&gb->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Fixed-order sum of n partials (stride between the K arrays = n) inside every CTA.
+template <int K>
+__device__ __forceinline__ void reduce_partials_all(const double* part, int n, double (&out)[K]) {
+  __shared__ double res[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[k] += __ldcg(part + k * n + q);
+  block_reduce<K>(out);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) res[k] = out[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = res[k];
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kTB, 4) k_pcg33_persistent(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+                                                             const double* __restrict__ minv, double* __restrict__ x,
+                                                             double* __restrict__ r, double* __restrict__ z,
+                                                             double* __restrict__ p, double* __restrict__ hp,
+                                                             PcgState* st, double* part, double* hist, GridBar* gb) {
+  constexpr int SW = kSpmvSW;
+  const int G = gridDim.x;
+  const int lane = threadIdx.x % SW;
+  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsw = int64_t(G) * blockDim.x / SW;
+  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
+  const double gnorm = st->gnorm;
+  const double tol = st->tol;
+  const long long max_iter = st->max_iter;
+  const long long hist_cap = st->hist_cap;
+  double rz = st->rz;
+  int status = st->status;
+  long long it = 0;
+  double rel = st->rel, php = 0.0, alpha = 0.0;
+  unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long t0 = gtimer();
+  while (status == 0) {
+    // ---- phase A: hp = H p, pHp partials
+    double dot[1] = {0.0};
+    for (int64_t R = sw0; R < nb; R += nsw) {
+      const RowPtrs p0 = load_rowptrs(S0, R);
+      RowPtrs p1{0, 0, 0, 0};
+      if (has1) p1 = load_rowptrs(S1, R);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      acc33<SW>(S0, p0, lane, p, a0, a1, a2);
+      if (has1) acc33<SW>(S1, p1, lane, p, a0, a1, a2);
+#pragma unroll
+      for (int off = SW / 2; off > 0; off >>= 1) {
+        a0 += __shfl_xor_sync(mask, a0, off, SW);
+        a1 += __shfl_xor_sync(mask, a1, off, SW);
+        a2 += __shfl_xor_sync(mask, a2, off, SW);
+      }
+      if (lane == 0) {
+        double* yo = hp + 3 * R;
+        yo[0] = a0;
+        yo[1] = a1;
+        yo[2] = a2;
+        dot[0] += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
+      }
+    }
+    block_reduce<1>(dot);
+    if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
+    grid_sync(gb);
+    unsigned long long t1 = gtimer();
+    ph[0] += t1 - t0;
+    t0 = t1;
+    double tot1[1];
+    reduce_partials_all<1>(part, G, tot1);
+    php = tot1[0];
+    if (!isfinite(php) || php <= 0.0) {
+      status = php == 0.0 ? 2 : 3;
+      break;
+    }
+    alpha = rz / php;
+    // ---- phase B: x += a p, r -= a hp, z = M^-1 r, partials of r.r and r.z
+    double v[2] = {0.0, 0.0};
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(G) * blockDim.x) {
+      const int64_t s0 = 3 * b;
+      double pp[3], hh[3], rr[3], xx[3], zz[3], M[9];
+      load_vec3(p + s0, pp[0], pp[1], pp[2]);
+      load_vec3_cg(hp + s0, hh[0], hh[1], hh[2]);
+      load_vec3(r + s0, rr[0], rr[1], rr[2]);
+      load_vec3(x + s0, xx[0], xx[1], xx[2]);
+      load_block9(minv + 9 * b, M);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xx[i] += alpha * pp[i];
+        rr[i] -= alpha * hh[i];
+      }
+      precond_apply<3>(M, rr, zz);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        x[s0 + i] = xx[i];
+        r[s0 + i] = rr[i];
+        z[s0 + i] = zz[i];
+        v[0] += rr[i] * rr[i];
+        v[1] += rr[i] * zz[i];
+      }
+    }
+    block_reduce<2>(v);
+    if (threadIdx.x == 0) {
+      part[G + blockIdx.x] = v[0];
+      part[2 * G + blockIdx.x] = v[1];
+    }
+    grid_sync(gb);
+    t1 = gtimer();
+    ph[1] += t1 - t0;
+    t0 = t1;
+    double tot2[2];
+    reduce_partials_all<2>(part + G, G, tot2);
+    t1 = gtimer();
+    ph[2] += t1 - t0;
+    t0 = t1;
+    rel = sqrt(tot2[0]) / gnorm;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it + 1 < hist_cap) hist[it + 1] = rel;
+    ++it;
+    if (!isfinite(rel)) {
+      status = 4;
+      break;
+    }
+    if (rel <= tol) {
+      status = 1;
+      break;
+    }
+    if (it >= max_iter) {
+      status = 5;
+      break;
+    }
+    const double beta = tot2[1] / rz;
+    rz = tot2[1];
+    // ---- phase C: p = z + beta p
+    {
+      const int64_t n2 = (3 * nb) >> 1;
+      const double2* z2 = reinterpret_cast<const double2*>(z);
+      double2* p2 = reinterpret_cast<double2*>(p);
+      for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(G) * blockDim.x) {
+        const double2 zz = __ldcg(z2 + i);
+        double2 q = p2[i];
+        q.x = zz.x + beta * q.x;
+        q.y = zz.y + beta * q.y;
+        p2[i] = q;
+      }
+      if (((3 * nb) & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[3 * nb - 1] = z[3 * nb - 1] + beta * p[3 * nb - 1];
+    }
+    grid_sync(gb);
+    t1 = gtimer();
+    ph[3] += t1 - t0;
+    t0 = t1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->it += it;
+    st->rel = rel;
+    st->rz = rz;
+    st->php = php;
+    st->alpha = alpha;
+    st->status = status;
+    if (status == 3 || status == 4) st->fail_it = int(it - (status == 4 ? 1 : 0));
+    for (int k = 0; k < 4; ++k) st->phase_ns[k] = ph[k];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -496,24 +786,13 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
   SpmvDev d0 = spmv_dev(s0);
   SpmvDev d1 = has1 ? spmv_dev(*s1) : d0;
   if (fast) {
-    static const int sw = [] {
-      const char* e = getenv("YS_SPMV_SW");
-      return e ? atoi(e) : 8;
-    }();
-    static int occ[3] = {0, 0, 0};
-    auto waves = [&](auto kern, int idx) {
-      if (!occ[idx]) {
-        YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[idx], kern, kTB, 0));
-        if (occ[idx] < 1) occ[idx] = 1;
-      }
-      // one resident wave, never more CTAs than the partial buffer holds
-      return std::min(grid, occ[idx] * sm_count());
-    };
-    switch (sw) {
-      case 4: k_spmv33<4><<<waves(k_spmv33<4>, 0), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
-      case 16: k_spmv33<16><<<waves(k_spmv33<16>, 2), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part); break;
-      default: k_spmv33<8><<<waves(k_spmv33<8>, 1), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
+    static int occ = 0;
+    if (!occ) {
+      YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv33, kTB, 0));
+      if (occ < 1) occ = 1;
     }
+    const int g = std::max(1, std::min(grid, occ * sm_count()));
+    k_spmv33<<<g, kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y, accumulate ? 1 : 0, st, part);
     YS_LAUNCH_CHECK();
     return;
   }
@@ -552,13 +831,24 @@ void ctx_apply_hessian_dev(Context& c, const double* x, double* y) {
   spmv_launch(c, c.S[0], &c.S[1], x, y, true, nullptr, nullptr, std::max(1, sm_count() * 8));
 }
 
+// Grids of the vector kernels: one thread per block row (update) or per
+// 16-byte pair (p-update), capped at one resident wave.
+static int vec_grid(Context& c, int64_t work) {
+  static int occ = 0;
+  if (!occ) {
+    YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update, kTB, 0));
+    if (occ < 1) occ = 1;
+  }
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, kTB), int64_t(occ) * sm_count())));
+}
+
 static void launch_iteration(Context& c, int grid, cudaGraphConditionalHandle h, bool use_cond) {
   PcgState* st = c.pcg.p;
   spmv_launch(c, c.S[0], &c.S[1], c.p.p, c.hp.p, false, st, c.partials.p, grid);
-  k_update<<<grid, kTB, 0, c.stream>>>(blocks_view(c), c.uniform3 ? 1 : 0, c.minv.p, c.DX.p, c.r.p, c.z.p, c.p.p,
-                                       c.hp.p, st, c.partials.p, c.hist.p);
+  k_update<<<vec_grid(c, c.NB), kTB, 0, c.stream>>>(blocks_view(c), c.uniform3 ? 1 : 0, c.minv.p, c.DX.p, c.r.p,
+                                                     c.z.p, c.p.p, c.hp.p, st, c.partials.p, c.hist.p);
   YS_LAUNCH_CHECK();
-  k_pupdate<<<grid, kTB, 0, c.stream>>>(c.s, c.z.p, c.p.p, st, h, use_cond ? 1 : 0);
+  k_pupdate<<<vec_grid(c, (c.s + 1) / 2), kTB, 0, c.stream>>>(c.s, c.z.p, c.p.p, st, h, use_cond ? 1 : 0);
   YS_LAUNCH_CHECK();
 }
 
@@ -649,6 +939,53 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
                                   c.pcg.p, c.partials.p, c.hist.p);
   YS_LAUNCH_CHECK();
 
+  // Uniform 3x3 systems: one persistent cooperative kernel runs the whole solve.
+  {
+    const bool has1 = c.S[1].n_blocks > 0;
+    const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
+    static const bool persistent_off = getenv("YS_PCG_PERSISTENT") && std::string(getenv("YS_PCG_PERSISTENT")) == "0";
+    if (fast && !persistent_off) {
+      static int occ = 0;
+      if (!occ) {
+        YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg33_persistent, kTB, 0));
+        if (occ < 1) occ = 1;
+      }
+      int gsz = occ * sm_count();
+      c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
+      c.gridbar.resize(sizeof(GridBar));
+      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
+      SpmvDev d0 = spmv_dev(c.S[0]);
+      SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+      int h1 = has1 ? 1 : 0;
+      int64_t nb = c.NB;
+      const double* minv = c.minv.p;
+      double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *part = c.partials.p,
+             *hist = c.hist.p;
+      PcgState* stp = c.pcg.p;
+      GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
+      void* args[] = {&d0, &d1, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
+      YS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg33_persistent), dim3(gsz), dim3(kTB), args, 0,
+                                          s));
+      PcgState fin{};
+      YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      YS_CUDA(cudaStreamSynchronize(s));
+      c.launches += 2;
+      for (int k = 0; k < 4; ++k) c.pcg_phase_ms[k] = double(fin.phase_ns[k]) * 1e-6;
+      c.hist_count = fin.status == 1 && fin.it == 0 && fin.gnorm == 0.0 ? 0 : fin.it + 1;
+      if (fin.status == 3)
+        fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
+                                   " (non-finite or negative curvature)");
+      if (fin.status == 4)
+        fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
+                                   " (non-finite residual)");
+      if (stats) {
+        stats->pcg_iterations = fin.it;
+        stats->pcg_converged = fin.status == 1 ? 1 : 0;
+        stats->pcg_residual = (fin.gnorm == 0.0) ? 0.0 : fin.rel;
+      }
+      return;
+    }
+  }
   // graph cache key: every pointer / flag the captured launches bake in
   Structure& s0 = c.S[0];
   Structure& s1 = c.S[1];

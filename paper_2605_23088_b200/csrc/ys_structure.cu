@@ -19,6 +19,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ys_device.cuh"
 
@@ -389,7 +390,7 @@ void build_structure_from_keys(Context& c, Structure& st, DevBuf<uint64_t>& keys
   }
   st.n_blocks = hsum->nu;
   st.n_values = hsum->n_values;
-  st.values.resize(size_t(st.n_values) + 2);  // +16 B: aligned-window loads of the last block
+  st.values.resize(size_t(st.n_values) + 4);  // +32 B: aligned-window loads of the last block
   st.values.n = size_t(st.n_values);
 }
 

@@ -398,7 +398,7 @@ class Engine:
         return ms.value, b.value
 
     def stage_times(self, with_counts: bool = False):
-        ms = np.zeros(8)
+        ms = np.zeros(12)
         cnt = np.zeros(2, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
         if with_counts:
