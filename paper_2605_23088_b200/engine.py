@@ -77,6 +77,72 @@ class HessianStructure:
                 yield (int(rows), int(cols), int(self.row[cs + k]), int(self.col[cs + k]),
                        self.values[vs + k * rows * cols: vs + (k + 1) * rows * cols].reshape(rows, cols))
 
+    def coordinate_entries(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """Scalar (row, col, value) entries, 0-based, in the storage order of
+        BlockSparseHessian::to_coordinate_text (assembly.cpp:106-134): block by
+        block, row-major inside a block, the strict lower part of diagonal
+        blocks skipped."""
+        rs, cs_, vs_ = [], [], []
+        for rows, cols, cst, cnt, vst in self.groups:
+            rows, cols, cnt = int(rows), int(cols), int(cnt)
+            if cnt == 0:
+                continue
+            r0 = self.row[cst:cst + cnt].astype(np.int64)
+            c0 = self.col[cst:cst + cnt].astype(np.int64)
+            a, b = np.divmod(np.arange(rows * cols), cols)
+            rr = r0[:, None] + a[None, :]
+            cc = c0[:, None] + b[None, :]
+            vv = self.values[vst:vst + cnt * rows * cols].reshape(cnt, rows * cols)
+            keep = ~((r0 == c0)[:, None] & (a > b)[None, :])
+            rs.append(rr[keep])
+            cs_.append(cc[keep])
+            vs_.append(vv[keep])
+        if not rs:
+            return np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0)
+        return np.concatenate(rs), np.concatenate(cs_), np.concatenate(vs_)
+
+    def to_coordinate_text(self) -> str:
+        """BlockSparseHessian::to_coordinate_text (assembly.cpp:106-134):
+        MatrixMarket coordinate text of the stored upper triangle, values at
+        17 significant digits."""
+        r, c, v = self.coordinate_entries()
+        return matrix_market_text(self.total_dofs, r, c, v)
+
+
+def matrix_market_text(total_dofs: int, r: np.ndarray, c: np.ndarray, v: np.ndarray) -> str:
+    """The header and entry lines both coordinate writers of the reference
+    emit (`os.precision(17)` prints a double like printf's %.17g)."""
+    head = ("%%MatrixMarket matrix coordinate real general\n% upper triangle of a symmetric matrix\n"
+            f"{total_dofs} {total_dofs} {len(v)}\n")
+    if len(v) == 0:
+        return head
+    flat = np.empty(3 * len(v), dtype=object)
+    flat[0::3] = (r + 1).tolist()
+    flat[1::3] = (c + 1).tolist()
+    flat[2::3] = v.tolist()
+    return head + ("%d %d %.17g\n" * len(v)) % tuple(flat)
+
+
+def merged_coordinate_text(eng: "Engine") -> str:
+    """merged_coordinate_text (sim.cpp:745-771), the `export-matrix` output: the
+    static and dynamic upper entries merged in a std::map keyed by (row, col).
+    Each map value starts at +0.0 and adds the static entry, then the dynamic
+    one, so -0.0 prints as 0 exactly as in the reference."""
+    parts = [eng.hessian(w).coordinate_entries() for w in (0, 1)]
+    r = np.concatenate([p[0] for p in parts])
+    c = np.concatenate([p[1] for p in parts])
+    v = np.concatenate([p[2] for p in parts])
+    order = np.lexsort((c, r))  # stable: static before dynamic for equal keys
+    r, c, v = r[order], c[order], v[order]
+    first = np.ones(len(v), dtype=bool)
+    first[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+    heads = np.flatnonzero(first)
+    acc = 0.0 + v[heads]
+    tail = np.flatnonzero(~first)  # blocks are unique per store: <= 1 dynamic entry per static key
+    seg = np.searchsorted(heads, tail, side="right") - 1
+    acc[seg] = acc[seg] + v[tail]
+    return matrix_market_text(eng.total_dofs(), r[heads], c[heads], acc)
+
 
 class Engine:
     def __init__(self, backend: str = "gpu", device: int = 0):

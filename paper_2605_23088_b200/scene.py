@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import json
 import math
+import os
+import sys
 import time
 from dataclasses import dataclass, field
 
@@ -391,6 +393,60 @@ class Simulation:
 
     def positions(self) -> list[np.ndarray]:
         return [self.body_positions(b) for b in self.bodies]
+
+    # -------------------------------------------------------------- output formats
+    def write_frame(self, os_, frame: int):
+        """Simulation::write_frame (sim.cpp:583-597): every body's "position"
+        output, 17 significant digits (printf %.17g)."""
+        os_.write(f"frame {frame}\n")
+        for b in self.bodies:
+            p = self.body_positions(b).reshape(-1, 3)
+            os_.write(f"body {b.name} position {len(p)} 3\n")
+            if len(p):
+                os_.write(("%.17g %.17g %.17g\n" * len(p)) % tuple(p.reshape(-1).tolist()))
+
+    def run(self, log=None):
+        """Simulation::run (sim.cpp:599-629): trajectory.txt and stats.csv under
+        output_dir, then the timing summary on `log`."""
+        log = log if log is not None else sys.stdout
+        cfg = self.config
+        try:
+            os.makedirs(cfg.output_dir, exist_ok=True)
+            traj = open(os.path.join(cfg.output_dir, "trajectory.txt"), "w")
+            stats = open(os.path.join(cfg.output_dir, "stats.csv"), "w")
+        except OSError:
+            raise _lib.ValidationError("cannot write to output directory " + cfg.output_dir)
+        with traj, stats:
+            stats.write("frame,newton,pcg,energy,max_step,pairs,nonincreasing\n")
+            diff_total = pcg_total = 0.0
+            newton_total = pcg_iters_total = 0
+            for f in range(1, cfg.frames + 1):
+                rep = self.step()
+                self.write_frame(traj, f)
+                stats.write("%d,%d,%d,%.17g,%.17g,%d,%d\n" % (f, rep.iterations, rep.pcg_iterations, rep.energy,
+                                                             rep.last_step_norm, self.pair_count(),
+                                                             1 if rep.energy_nonincreasing else 0))
+                diff_total += rep.diff_seconds
+                pcg_total += rep.pcg_seconds
+                newton_total += rep.iterations
+                pcg_iters_total += rep.pcg_iterations
+        log.write("frames %d\n" % cfg.frames
+                  + "diff total (s) %g\n" % diff_total
+                  + "diff average (ms) %g\n" % (1e3 * diff_total / newton_total if newton_total else 0.0)
+                  + "cg total (s) %g\n" % pcg_total
+                  + "cg average (ms) %g\n" % (1e3 * pcg_total / pcg_iters_total if pcg_iters_total else 0.0)
+                  + "newton iterations %d\n" % newton_total
+                  + "cg iterations %d\n" % pcg_iters_total)
+
+    def export_matrix(self, frame: int = 0) -> str:
+        """The `export-matrix` subcommand (sim.cpp:848-861): step `frame` frames,
+        refresh + assemble(project=true), merged MatrixMarket text."""
+        from .engine import merged_coordinate_text
+        for _ in range(frame):
+            self.step()
+        self.eng.refresh_dynamic()
+        self.eng.assemble(True)
+        return merged_coordinate_text(self.eng)
 
 
 def load_obj(path: str):
