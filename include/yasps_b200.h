@@ -223,6 +223,36 @@ int ys_bsr_pcg(ys_context* ctx, int32_t bsr, int32_t bs, const double* g, double
                int32_t* converged);
 
 /* ------------------------------------------------------------------------
+ * Multi-GPU: row-partitioned PCG, one process per GPU.
+ * Every rank registers the same scene, so structures, evaluation and assembly
+ * are replicated; minimize_step then solves with each rank owning a
+ * contiguous range of block rows (balanced by stored entries), exchanging the
+ * halo of p once per iteration and the dot-product partials of every rank
+ * twice per iteration.  Partials are summed in rank order on every rank, so
+ * all ranks hold bit-identical alpha / beta / status and stop together; the
+ * result is deterministic for a fixed rank count.  At the end dx is gathered
+ * so every rank returns the full step (the reference's Engine::minimize_step
+ * contract, engine.cpp:75-101).  Uniform 3x3 block systems only.
+ *
+ * The transport is one primitive: allgather of `count` doubles per rank into
+ * nranks * count (rank-major).  YS NCCL transport: ncclAllGather on the
+ * context stream (libnccl.so.2 is dlopen-ed, no link dependency).  Host
+ * transport: a caller callback over HOST buffers (e.g. torch.distributed
+ * gloo), used by the multi-process tests on one device.
+ * ------------------------------------------------------------------------ */
+typedef int (*ys_allgather_fn)(void* user, const double* send, double* recv, int64_t count);
+/* ncclGetUniqueId; rank 0 creates it and the caller broadcasts the 128 bytes. */
+int ys_dist_unique_id(unsigned char id[128]);
+int ys_dist_init_nccl(ys_context* ctx, int32_t rank, int32_t nranks, const unsigned char id[128]);
+int ys_dist_init_host(ys_context* ctx, int32_t rank, int32_t nranks, ys_allgather_fn fn, void* user);
+/* Back to single-GPU solves (destroys the NCCL communicator). */
+int ys_dist_finalize(ys_context* ctx);
+/* The partition of the last distributed solve: bounds (nranks + 1 block-row
+ * boundaries), this rank's halo rows received per iteration, export rows sent. */
+int ys_dist_info(ys_context* ctx, int32_t* rank, int32_t* nranks, int64_t* bounds, int64_t* halo_rows,
+                 int64_t* export_rows);
+
+/* ------------------------------------------------------------------------
  * Benchmark hooks: per-stage device times of the last minimize_step, measured
  * with CUDA events on the context's stream (ms): [0] refresh_dynamic,
  * [1] local eval, [2] assembly gather, [3] preconditioner build, [4] PCG,

@@ -159,6 +159,11 @@ struct yo_context {
   /* free-standing systems */
   Bsr* sys;
   int nsys;
+  /* row-partitioned solve (restatement of ys_dist.cu) */
+  int dist_on, dist_rank, dist_n;
+  ys_allgather_fn dist_fn;
+  void* dist_user;
+  int64_t dist_bounds[65], dist_exp_off[65];
 };
 
 /* ------------------------------------------------------------------------ */
@@ -1170,6 +1175,205 @@ static void pcg(yo_context* c, Bsr* h0, Bsr* h1, const double* g, double tol, in
 }
 
 /* ------------------------------------------------------------------------
+ * Row-partitioned PCG over nranks processes (the algorithm of
+ * ys_dist.cu restated serially per rank).  Partition: W(R) = entries of block
+ * rows < R (each upper block once at its row, off-diagonal blocks once more
+ * at their column row, both stores) + R; bounds[k] = first R with
+ * W(R) >= k W(NB) / n.  Halo: a block (R, C) with owner(R) != owner(C)
+ * exports rows R and C.  Dot products: the rank's partial over its rows in
+ * row order, then the allgathered partials summed in rank order.
+ * ------------------------------------------------------------------------ */
+static int owner_of(const int64_t* bounds, int n, int64_t v) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (bounds[mid] <= v) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+static void dist_gather(yo_context* c, const double* send, double* recv, int64_t count) {
+  if (c->dist_fn(c->dist_user, send, recv, count) != 0)
+    fail(c, YS_ERR_CUDA, "distributed solve: the host allgather callback failed");
+}
+
+static void dist_spmv_rows(const Bsr* h, int64_t a, int64_t b, const double* x, double* y) {
+  for (int64_t bi = 0; bi < h->nb; ++bi) {
+    const double* B = h->values + h->voff[bi];
+    const int64_t r = h->row[bi], cc = h->col[bi];
+    if (r / 3 >= a && r / 3 < b)
+      for (int i = 0; i < 3; ++i) y[r + i] += B[3 * i] * x[cc] + B[3 * i + 1] * x[cc + 1] + B[3 * i + 2] * x[cc + 2];
+    if (r != cc && cc / 3 >= a && cc / 3 < b)
+      for (int j = 0; j < 3; ++j) y[cc + j] += B[j] * x[r] + B[3 + j] * x[r + 1] + B[6 + j] * x[r + 2];
+  }
+}
+
+static void dist_pcg(yo_context* c, double tol, int64_t max_iter, double* x, int64_t* iters, double* relres,
+                     int* converged) {
+  const int n = c->dist_n, me = c->dist_rank;
+  const int64_t NB = c->nblk, s = c->s;
+  for (int64_t b = 0; b < NB; ++b)
+    if (c->brc[b] != 3) fail(c, YS_ERR_VALIDATION, "distributed PCG supports uniform 3x3 block systems only");
+  /* partition */
+  int64_t* W = xcalloc((size_t)NB + 1, sizeof(int64_t));
+  for (int w = 0; w < 2; ++w)
+    for (int64_t bi = 0; bi < c->H[w].nb; ++bi) {
+      W[c->H[w].row[bi] / 3 + 1] += 1;
+      if (c->H[w].row[bi] != c->H[w].col[bi]) W[c->H[w].col[bi] / 3 + 1] += 1;
+    }
+  for (int64_t R = 0; R < NB; ++R) W[R + 1] += W[R] + 1;
+  int64_t* bounds = c->dist_bounds;
+  bounds[0] = 0;
+  bounds[n] = NB;
+  for (int k = 1; k < n; ++k) {
+    const int64_t target = W[NB] * k / n;
+    int64_t lo = 0, hi = NB;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (W[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    bounds[k] = lo;
+  }
+  free(W);
+  /* halo */
+  unsigned char* need = xcalloc((size_t)NB, 1);
+  for (int w = 0; w < 2; ++w)
+    for (int64_t bi = 0; bi < c->H[w].nb; ++bi) {
+      const int64_t R = c->H[w].row[bi] / 3, C = c->H[w].col[bi] / 3;
+      if (R != C && owner_of(bounds, n, R) != owner_of(bounds, n, C)) need[R] = need[C] = 1;
+    }
+  int64_t nexp = 0;
+  int64_t* exp = xcalloc((size_t)NB + 1, sizeof(int64_t));
+  for (int64_t R = 0; R < NB; ++R)
+    if (need[R]) exp[nexp++] = R;
+  free(need);
+  int64_t* off = c->dist_exp_off;
+  for (int k = 0; k <= n; ++k) {
+    int64_t lo = 0, hi = nexp;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (exp[mid] < bounds[k]) lo = mid + 1;
+      else hi = mid;
+    }
+    off[k] = lo;
+  }
+  int64_t maxe = 0, maxr = 0;
+  for (int k = 0; k < n; ++k) {
+    if (off[k + 1] - off[k] > maxe) maxe = off[k + 1] - off[k];
+    if (bounds[k + 1] - bounds[k] > maxr) maxr = bounds[k + 1] - bounds[k];
+  }
+  const int64_t a = bounds[me], b = bounds[me + 1];
+  const int64_t big = 3 * (maxe > maxr ? maxe : maxr) + 2;
+  double* send = xcalloc((size_t)big, sizeof(double));
+  double* recv = xcalloc((size_t)big * (size_t)n, sizeof(double));
+  double* r = xcalloc((size_t)s, sizeof(double));
+  double* z = xcalloc((size_t)s, sizeof(double));
+  double* p = xcalloc((size_t)s, sizeof(double));
+  double* hp = xcalloc((size_t)s, sizeof(double));
+  double part[2], all[128];
+  memset(x, 0, sizeof(double) * (size_t)s);
+  free(c->hist);
+  c->hist = xcalloc((size_t)(max_iter + 2), sizeof(double));
+  c->hist_n = 0;
+  *iters = 0;
+  *relres = 0.0;
+  *converged = 0;
+  /* r = g, z = M^-1 r, p = z on owned rows */
+  part[0] = part[1] = 0.0;
+  for (int64_t R = a; R < b; ++R) {
+    const double* M = c->minv + c->bvoff[R];
+    for (int i = 0; i < 3; ++i) r[3 * R + i] = c->G[3 * R + i];
+    for (int i = 0; i < 3; ++i) {
+      z[3 * R + i] = M[3 * i] * r[3 * R] + M[3 * i + 1] * r[3 * R + 1] + M[3 * i + 2] * r[3 * R + 2];
+      p[3 * R + i] = z[3 * R + i];
+      part[0] += r[3 * R + i] * r[3 * R + i];
+      part[1] += r[3 * R + i] * z[3 * R + i];
+    }
+  }
+  dist_gather(c, part, all, 2);
+  double gg = 0.0, rz = 0.0;
+  for (int k = 0; k < n; ++k) {
+    gg += all[2 * k];
+    rz += all[2 * k + 1];
+  }
+  const double gnorm = sqrt(gg);
+  int status = gnorm == 0.0 ? 1 : (max_iter > 0 ? 0 : 5);
+  if (gnorm != 0.0) c->hist[c->hist_n++] = 1.0;
+  else *converged = 1;
+  int64_t it = 0;
+  while (status == 0) {
+    if (maxe > 0) { /* halo of p */
+      const int64_t mine = off[me + 1] - off[me];
+      for (int64_t i = 0; i < mine; ++i)
+        for (int d = 0; d < 3; ++d) send[3 * i + d] = p[3 * exp[off[me] + i] + d];
+      dist_gather(c, send, recv, 3 * maxe);
+      for (int k = 0; k < n; ++k) {
+        if (k == me) continue;
+        for (int64_t e = off[k]; e < off[k + 1]; ++e)
+          for (int d = 0; d < 3; ++d) p[3 * exp[e] + d] = recv[(k * maxe + (e - off[k])) * 3 + d];
+      }
+    }
+    memset(hp, 0, sizeof(double) * (size_t)s);
+    dist_spmv_rows(&c->H[0], a, b, p, hp);
+    dist_spmv_rows(&c->H[1], a, b, p, hp);
+    part[0] = 0.0;
+    for (int64_t i = 3 * a; i < 3 * b; ++i) part[0] += p[i] * hp[i];
+    dist_gather(c, part, all, 1);
+    double php = 0.0;
+    for (int k = 0; k < n; ++k) php += all[k];
+    if (!isfinite(php) || php <= 0.0) {
+      if (php == 0.0) break;
+      fail(c, YS_ERR_NUMERICAL, "PCG diverged at iteration %lld (non-finite or negative curvature)", (long long)it);
+    }
+    const double alpha = rz / php;
+    part[0] = part[1] = 0.0;
+    for (int64_t R = a; R < b; ++R) {
+      const double* M = c->minv + c->bvoff[R];
+      for (int i = 0; i < 3; ++i) {
+        x[3 * R + i] += alpha * p[3 * R + i];
+        r[3 * R + i] -= alpha * hp[3 * R + i];
+      }
+      for (int i = 0; i < 3; ++i) {
+        z[3 * R + i] = M[3 * i] * r[3 * R] + M[3 * i + 1] * r[3 * R + 1] + M[3 * i + 2] * r[3 * R + 2];
+        part[0] += r[3 * R + i] * r[3 * R + i];
+        part[1] += r[3 * R + i] * z[3 * R + i];
+      }
+    }
+    dist_gather(c, part, all, 2);
+    double rr = 0.0, rzn = 0.0;
+    for (int k = 0; k < n; ++k) {
+      rr += all[2 * k];
+      rzn += all[2 * k + 1];
+    }
+    const double rel = sqrt(rr) / gnorm;
+    *iters = ++it;
+    c->hist[c->hist_n++] = rel;
+    if (!isfinite(rel))
+      fail(c, YS_ERR_NUMERICAL, "PCG diverged at iteration %lld (non-finite residual)", (long long)(it - 1));
+    if (rel <= tol) {
+      *converged = 1;
+      break;
+    }
+    if (it >= max_iter) break;
+    const double beta = rzn / rz;
+    rz = rzn;
+    for (int64_t i = 3 * a; i < 3 * b; ++i) p[i] = z[i] + beta * p[i];
+  }
+  if (c->hist_n) *relres = c->hist[c->hist_n - 1];
+  if (n > 1) { /* every rank returns the full step */
+    for (int64_t i = 0; i < 3 * (b - a); ++i) send[i] = x[3 * a + i];
+    dist_gather(c, send, recv, 3 * maxr);
+    for (int64_t R = 0; R < NB; ++R) {
+      const int k = owner_of(bounds, n, R);
+      for (int d = 0; d < 3; ++d) x[3 * R + d] = recv[(k * maxr + (R - bounds[k])) * 3 + d];
+    }
+  }
+  free(exp); free(send); free(recv); free(r); free(z); free(p); free(hp);
+}
+
+/* ------------------------------------------------------------------------
  * Engine construction (engine.cpp:7-20)
  * ------------------------------------------------------------------------ */
 static void finalize(yo_context* c) {
@@ -1733,7 +1937,8 @@ int yo_minimize_step(yo_context* c, double tol, int64_t max_iter, double* dx, ys
   int64_t it;
   double rel;
   int conv;
-  pcg(c, &c->H[0], &c->H[1], c->G, tol, max_iter, c->DX, &it, &rel, &conv);
+  if (c->dist_on) dist_pcg(c, tol, max_iter, c->DX, &it, &rel, &conv);
+  else pcg(c, &c->H[0], &c->H[1], c->G, tol, max_iter, c->DX, &it, &rel, &conv);
   memcpy(c->X0, c->X, sizeof(double) * (size_t)c->s);
   if (dx) memcpy(dx, c->DX, sizeof(double) * (size_t)c->s);
   if (stats) {
@@ -1989,5 +2194,47 @@ int yo_bsr_pcg(yo_context* c, int32_t id, int32_t bs, const double* g, double to
   if (iters) *iters = it;
   if (rel) *rel = rr;
   if (conv) *conv = cv;
+  API_END;
+}
+
+/* multi-rank solve entry points (ys_dist_init_host / finalize / info) */
+int yo_dist_init_host(yo_context* c, int32_t rank, int32_t nranks, ys_allgather_fn fn, void* user) {
+  API_BEGIN(c);
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks)
+    fail(c, YS_ERR_VALIDATION, "distributed solve: rank %d of %d is out of range (1..64 ranks)", rank, nranks);
+  if (!fn) fail(c, YS_ERR_VALIDATION, "distributed solve: null allgather callback");
+  c->dist_on = 1;
+  c->dist_rank = rank;
+  c->dist_n = nranks;
+  c->dist_fn = fn;
+  c->dist_user = user;
+  c->dist_bounds[0] = 0;
+  c->dist_bounds[1] = c->nblk;
+  memset(c->dist_exp_off, 0, sizeof(c->dist_exp_off));
+  API_END;
+}
+
+int yo_dist_finalize(yo_context* c) {
+  API_BEGIN(c);
+  c->dist_on = 0;
+  API_END;
+}
+
+int yo_dist_info(yo_context* c, int32_t* rank, int32_t* nranks, int64_t* bounds, int64_t* halo_rows,
+                 int64_t* export_rows) {
+  API_BEGIN(c);
+  const int n = c->dist_on ? c->dist_n : 1;
+  if (rank) *rank = c->dist_on ? c->dist_rank : 0;
+  if (nranks) *nranks = n;
+  if (bounds) {
+    if (c->dist_on) memcpy(bounds, c->dist_bounds, sizeof(int64_t) * (size_t)(n + 1));
+    else {
+      bounds[0] = 0;
+      bounds[1] = c->nblk;
+    }
+  }
+  const int64_t mine = c->dist_on ? c->dist_exp_off[c->dist_rank + 1] - c->dist_exp_off[c->dist_rank] : 0;
+  if (halo_rows) *halo_rows = c->dist_on ? c->dist_exp_off[n] - mine : 0;
+  if (export_rows) *export_rows = mine;
   API_END;
 }

@@ -72,6 +72,8 @@ _PI32 = C.POINTER(C.c_int32)
 _PI64 = C.POINTER(C.c_int64)
 _PU64 = C.POINTER(C.c_uint64)
 _PD = C.POINTER(C.c_double)
+# ys_allgather_fn: int (*)(void* user, const double* send, double* recv, int64_t count)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, _PD, _PD, C.c_int64)
 
 # name -> argtypes (all return int status unless listed in _RESTYPES)
 _SIGS = {
@@ -133,11 +135,17 @@ _SIGS = {
     "bump_dynamic_epoch": [_P],
     "stream": [_P, C.POINTER(C.c_void_p)],
     "time_kernel": [_P, _I32, _I32, _PD, _PD],
+    "dist_unique_id": [C.c_char_p],
+    "dist_init_nccl": [_P, _I32, _I32, C.c_char_p],
+    "dist_init_host": [_P, _I32, _I32, ALLGATHER_FN, _P],
+    "dist_finalize": [_P],
+    "dist_info": [_P, _PI32, _PI32, _PI64, _PI64, _PI64],
 }
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
-OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream"}
+OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream", "dist_unique_id",
+            "dist_init_nccl"}
 
 
 class Library:

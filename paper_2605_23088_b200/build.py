@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-diag-suppress", "177", "-I", str(INCLUDE)]
-SOURCES = ["ys_structure.cu", "ys_assemble.cu", "ys_solver.cu", "ys_capi.cu"]
+SOURCES = ["ys_structure.cu", "ys_assemble.cu", "ys_solver.cu", "ys_dist.cu", "ys_capi.cu"]
 
 
 def _deps() -> list[Path]:
@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         for lg in logs:
             sys.stderr.write(lg)
     if force or jobs or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs), "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -408,6 +408,10 @@ void ys_destroy(ys_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   drop_pcg_graph(*c);
+  try {
+    ctx_dist_finalize(*c);
+  } catch (...) {
+  }
   for (auto& sub : c->subs) drop_pcg_graph(*sub);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& sub : c->subs)
@@ -840,7 +844,8 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));
     if (max_iter < 0) max_iter = std::max<int64_t>(2 * c->s, 64);
     ys_step_stats local{};
-    ctx_pcg(*c, tol, max_iter, c->G.p, c->DX.p, &local);
+    if (c->dist.kind) ctx_dist_pcg(*c, tol, max_iter, &local);
+    else ctx_pcg(*c, tol, max_iter, c->G.p, c->DX.p, &local);
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[6], c->stream));
     YS_CUDA(cudaMemcpyAsync(c->X0.p, c->X.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     if (dx) c->DX.download(dx, size_t(c->s), c->stream);
@@ -1139,6 +1144,68 @@ int ys_bsr_pcg(ys_context* c, int32_t id, int32_t bs, const double* g, double to
 
 int ys_bump_dynamic_epoch(ys_context* c) {
   return guarded(c, [&] { ++c->epoch; });
+}
+
+int ys_dist_unique_id(unsigned char id[128]) {
+  try {
+    ctx_dist_unique_id(id);
+    return YS_OK;
+  } catch (const ys::Error& e) {
+    return e.cls;
+  }
+}
+
+static void check_ranks(int32_t rank, int32_t nranks) {
+  if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks)
+    fail(YS_ERR_VALIDATION, "distributed solve: rank " + std::to_string(rank) + " of " + std::to_string(nranks) +
+                                " is out of range (1..64 ranks)");
+}
+
+int ys_dist_init_nccl(ys_context* c, int32_t rank, int32_t nranks, const unsigned char id[128]) {
+  return guarded(c, [&] {
+    check_ranks(rank, nranks);
+    ctx_dist_finalize(*c);
+    c->dist.rank = rank;
+    c->dist.nranks = nranks;
+    ctx_dist_init_nccl(*c, rank, nranks, id);
+  });
+}
+
+int ys_dist_init_host(ys_context* c, int32_t rank, int32_t nranks, ys_allgather_fn fn, void* user) {
+  return guarded(c, [&] {
+    check_ranks(rank, nranks);
+    if (!fn) fail(YS_ERR_VALIDATION, "distributed solve: null allgather callback");
+    ctx_dist_finalize(*c);
+    c->dist.rank = rank;
+    c->dist.nranks = nranks;
+    c->dist.fn = fn;
+    c->dist.user = user;
+    c->dist.kind = 1;
+  });
+}
+
+int ys_dist_finalize(ys_context* c) {
+  return guarded(c, [&] { ctx_dist_finalize(*c); });
+}
+
+int ys_dist_info(ys_context* c, int32_t* rank, int32_t* nranks, int64_t* bounds, int64_t* halo_rows,
+                 int64_t* export_rows) {
+  return guarded(c, [&] {
+    const DistState& d = c->dist;
+    if (rank) *rank = d.kind ? d.rank : 0;
+    if (nranks) *nranks = d.kind ? d.nranks : 1;
+    const bool have = d.kind && int(d.bounds.size()) == d.nranks + 1;
+    if (bounds) {
+      if (have) std::copy(d.bounds.begin(), d.bounds.end(), bounds);
+      else {
+        bounds[0] = 0;
+        bounds[1] = c->NB;
+      }
+    }
+    const int64_t mine = have ? d.exp_off[d.rank + 1] - d.exp_off[d.rank] : 0;
+    if (halo_rows) *halo_rows = have ? d.exp_off[d.nranks] - mine : 0;
+    if (export_rows) *export_rows = mine;
+  });
 }
 
 int ys_stream(ys_context* c, void** stream) {

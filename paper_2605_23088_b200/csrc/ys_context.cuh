@@ -135,6 +135,25 @@ struct PcgState {
   unsigned long long phase_ns[4];  // persistent PCG: SpMV+pHp, reduce+update, reduce, p-update (CTA 0 view)
 };
 
+// Row-partitioned multi-GPU solve (ys_dist.cu).  The plan is rebuilt per
+// solve because the dynamic structure changes every Newton iteration.
+struct DistState {
+  int kind = 0;  // 0 off, 1 host callback transport, 2 NCCL
+  int rank = 0, nranks = 1;
+  ys_allgather_fn fn = nullptr;
+  void* user = nullptr;
+  void* nccl = nullptr;               // ncclComm_t
+  std::vector<int64_t> bounds;        // nranks + 1 block-row boundaries (last solve)
+  std::vector<int64_t> exp_off;       // nranks + 1 offsets into the export list
+  int64_t max_exp = 0, max_rows = 0;  // padded allgather sizes (rows)
+  DevBuf<int64_t> dbounds, dexp_off;
+  DevBuf<uint8_t> need;               // NB: row referenced across a rank boundary
+  DevBuf<int32_t> exp;                // export rows of all ranks, sorted
+  DevBuf<int32_t> nsel;
+  DevBuf<double> send, recv, dsend, dall;
+  std::vector<double> hsend, hrecv;   // host transport staging
+};
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -207,6 +226,8 @@ struct Context {
   int64_t launches = 0;
   cudaEvent_t ev[10] = {};
 
+  DistState dist;
+
   // free-standing BSR systems (ys_bsr_*)
   struct Bsr {
     int64_t s = 0;
@@ -228,6 +249,10 @@ void ctx_build_preconditioner(Context& c);
 void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev,
              ys_step_stats* stats);
 void ctx_upload_domains(Context& c);
+void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats);
+void ctx_dist_unique_id(unsigned char* id);
+void ctx_dist_init_nccl(Context& c, int rank, int nranks, const unsigned char* id);
+void ctx_dist_finalize(Context& c);
 uint64_t structure_checksum(Context& c, Structure& st, int64_t total_dofs);
 void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed,
                        int64_t* n_pairs);

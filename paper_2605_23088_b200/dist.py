@@ -1,0 +1,54 @@
+"""One process per GPU: wiring the engine's row-partitioned PCG to
+torch.distributed.
+
+`init_nccl(eng)` is the production path: rank 0 asks the library for an NCCL
+unique id, the process group broadcasts it, and the library then runs its own
+ncclAllGather on the engine's stream.  `init_host(eng)` routes the same
+allgather through torch.distributed on host buffers — any backend, used by the
+multi-process tests (gloo, several ranks sharing one device)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+def unique_id(backend: str = "gpu") -> bytes:
+    lib = _lib.gpu_library() if backend == "gpu" else _lib.oracle_library()
+    if not lib.has("dist_unique_id"):
+        raise _lib.DeclError(f"{lib.path.name} has no NCCL transport")
+    buf = C.create_string_buffer(128)
+    st = lib.fns["dist_unique_id"](buf)
+    if st != 0:
+        raise _lib.CudaError("ncclGetUniqueId failed (is libnccl.so.2 loadable?)")
+    return buf.raw
+
+
+def init_nccl(eng, group=None):
+    import torch
+    import torch.distributed as dist
+    rank, n = dist.get_rank(group), dist.get_world_size(group)
+    uid = unique_id(eng.backend) if rank == 0 else bytes(128)
+    t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).clone()
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, 0, group=group)
+    eng.dist_init_nccl(rank, n, bytes(t.cpu().numpy().tobytes()))
+
+
+def torch_allgather(group=None):
+    """allgather(send, recv) over torch.distributed on host tensors."""
+    import torch
+    import torch.distributed as dist
+
+    def ag(send: np.ndarray, recv: np.ndarray):
+        outs = [torch.from_numpy(recv[k]) for k in range(recv.shape[0])]
+        dist.all_gather(outs, torch.from_numpy(np.ascontiguousarray(send)), group=group)
+    return ag
+
+
+def init_host(eng, group=None):
+    import torch.distributed as dist
+    eng.dist_init_host(dist.get_rank(group), dist.get_world_size(group), torch_allgather(group))

@@ -350,6 +350,45 @@ class Engine:
         return Step(dx, st.pcg_iterations, st.pcg_residual, bool(st.pcg_converged), st.regularized_blocks,
                     st.assemble_seconds, st.solve_seconds)
 
+    # ---------------- multi-GPU (row-partitioned PCG) ----------------
+    def dist_init_nccl(self, rank: int, nranks: int, unique_id: bytes):
+        """Solve with this rank's block rows, NCCL allgather on the engine's stream.
+        unique_id: 128 bytes from dist_unique_id() on rank 0, broadcast by the caller."""
+        if not self.lib.has("dist_init_nccl"):
+            raise _lib.DeclError(f"{self.lib.path.name} has no NCCL transport")
+        if len(unique_id) != 128:
+            raise _lib.ValidationError("NCCL unique id must be 128 bytes")
+        self._c(self.f["dist_init_nccl"](self.ctx, int(rank), int(nranks), bytes(unique_id)))
+
+    def dist_init_host(self, rank: int, nranks: int, allgather):
+        """Host transport: allgather(send (count,), recv (nranks, count)) fills recv
+        rank-major from every rank's send (e.g. torch.distributed over gloo)."""
+        def cb(_user, send, recv, count):
+            try:
+                s = np.ctypeslib.as_array(send, shape=(int(count),)) if count else np.zeros(0)
+                r = np.ctypeslib.as_array(recv, shape=(int(nranks) * int(count),)) if count else np.zeros(0)
+                allgather(s, r.reshape(int(nranks), int(count)))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status through the C-ABI
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._dist_cb = _lib.ALLGATHER_FN(cb)  # keep the thunk alive
+        self._c(self.f["dist_init_host"](self.ctx, int(rank), int(nranks), self._dist_cb, None))
+
+    def dist_finalize(self):
+        self._c(self.f["dist_finalize"](self.ctx))
+        self._dist_cb = None
+
+    def dist_info(self) -> dict:
+        rank, nranks = C.c_int32(), C.c_int32()
+        bounds = np.zeros(65, dtype=np.int64)
+        halo, exp = C.c_int64(), C.c_int64()
+        self._c(self.f["dist_info"](self.ctx, C.byref(rank), C.byref(nranks), bounds.ctypes.data_as(_lib._PI64),
+                                    C.byref(halo), C.byref(exp)))
+        return {"rank": rank.value, "nranks": nranks.value, "bounds": bounds[:nranks.value + 1].copy(),
+                "halo_rows": halo.value, "export_rows": exp.value}
+
     def split_per_target(self, flat: np.ndarray) -> list[np.ndarray]:
         out, off = [], 0
         for n, rc in self.targets:

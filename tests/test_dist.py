@@ -1,0 +1,114 @@
+"""Row-partitioned multi-rank PCG, one process per rank over
+torch.distributed gloo.
+
+CPU: the oracle's restatement of the partition / halo / rank-ordered-sum
+algorithm at 2 and 3 ranks against its own single-rank solve.
+GPU: the library with 2 ranks sharing cuda:0 (host transport) against the
+single-GPU solve and against the oracle's partition (bit-exact bounds and
+halo sizes); NCCL transport at 1 rank (the only rank count one device runs)."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _scene(backend):
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+    sim = Simulation(SimConfig.from_dict(configs.c1()), backend=backend)
+    configs.jitter_targets(sim, 0.0025)
+    sim.begin_frame()
+    sim.refresh_dynamic_pairs()
+    return sim
+
+
+def _worker(rank, world, port, backend, transport, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_23088_b200 import dist as ysdist
+        sim = _scene(backend)
+        if transport == "nccl":
+            ysdist.init_nccl(sim.eng)
+        else:
+            ysdist.init_host(sim.eng)
+        st = sim.eng.minimize_step(1e-4)
+        info = sim.eng.dist_info()
+        out.put((rank, st.pcg_iterations, st.pcg_converged, st.dx, info))
+    except Exception as e:  # surface worker failures to the test
+        out.put((rank, "error", repr(e), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, backend, transport="host"):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() * 7 + world) % 1000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, transport, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=600)
+        assert r[1] != "error", r[2]
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+    return [res[k] for k in range(world)]
+
+
+def _single(backend):
+    sim = _scene(backend)
+    st = sim.eng.minimize_step(1e-4)
+    return st, sim.eng.s
+
+
+def _check(results, ref, world):
+    st_ref, s = ref
+    dx_ref = st_ref.dx
+    for rank, it, conv, dx, info in results:
+        assert info["rank"] == rank and info["nranks"] == world
+        assert it == st_ref.pcg_iterations and conv == st_ref.pcg_converged
+        # every rank returns the same full step, bit for bit
+        assert np.array_equal(dx, results[0][3])
+        assert np.max(np.abs(dx - dx_ref)) <= 1e-10 * np.max(np.abs(dx_ref))
+    b = results[0][4]["bounds"]
+    assert b[0] == 0 and b[-1] == s // 3 and np.all(np.diff(b) > 0)
+    for r in results:
+        assert np.array_equal(r[4]["bounds"], b)
+    if world > 1:
+        assert all(r[4]["halo_rows"] > 0 and r[4]["export_rows"] > 0 for r in results)
+        # every row a rank exports is received by the others
+        assert sum(r[4]["export_rows"] for r in results) == results[0][4]["halo_rows"] + results[0][4]["export_rows"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_pcg_oracle(world):
+    _check(_run(world, "oracle"), _single("oracle"), world)
+
+
+@pytest.mark.gpu
+def test_row_partitioned_pcg_gpu_two_ranks():
+    gpu = _run(2, "gpu")
+    _check(gpu, _single("gpu"), 2)
+    ora = _run(2, "oracle")
+    for g, o in zip(gpu, ora):  # same partition and halo, bit for bit
+        assert np.array_equal(g[4]["bounds"], o[4]["bounds"])
+        assert g[4]["halo_rows"] == o[4]["halo_rows"] and g[4]["export_rows"] == o[4]["export_rows"]
+        assert g[1] == o[1]
+        assert np.max(np.abs(g[3] - o[3])) <= 1e-9 * np.max(np.abs(o[3]))
+
+
+@pytest.mark.gpu
+def test_nccl_transport_single_rank():
+    _check(_run(1, "gpu", "nccl"), _single("gpu"), 1)
