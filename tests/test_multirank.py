@@ -1,7 +1,6 @@
-"""world_size-2 gloo test of the N>1 path (CPU): every rank runs its own
-replica of the scene step (bench.py --gpus N semantics, "replicas only"
-until the row-partitioned PCG lands) and the max-over-ranks timing /
-result reduction agrees."""
+"""world_size-2 gloo test of bench.py's rank plumbing (CPU): identical scene
+replicas on every rank and the max-over-ranks reduction the bench uses for
+its timing.  The row-partitioned solve itself is tested in test_dist.py."""
 from __future__ import annotations
 
 import os
