@@ -11,8 +11,9 @@ Newton iteration because each pair refresh bumps the dynamic epoch).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
 
-N > 1 (torchrun): one independent replica of the scene per GPU ("weak";
-the row-partitioned multi-GPU PCG is not built yet).
+N > 1 (torchrun): the same scene on every rank, solved by the row-partitioned
+multi-GPU PCG over NCCL ("strong": evaluation and assembly replicated, the PCG
+rows split across ranks).
 """
 from __future__ import annotations
 
@@ -124,12 +125,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def traffic_from_profiles(scene: str):
-    """dram bytes per launch of the SpMV kernel from the committed ncu capture."""
+def traffic_from_profiles(scene: str, key: str):
+    """DRAM bytes (read + write) from the committed ncu capture (profiles/ncu_summary.json):
+    "pcg_dram_bytes_per_iteration" of the persistent PCG kernel, "spmv_dram_bytes" per SpMV launch."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d.get(scene, {}).get("spmv_dram_bytes")
+        return d.get(scene, {}).get(key)
     except Exception:
         return None
 
@@ -216,6 +218,9 @@ def main():
     from paper_2605_23088_b200 import _lib
     sim = prepare(args.config, bool(args.via_f), "gpu", local)
     eng = sim.eng
+    if world > 1:
+        from paper_2605_23088_b200 import dist as ysdist
+        ysdist.init_nccl(eng)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", local))
     cfg = sim.config
 
@@ -257,6 +262,14 @@ def main():
     eval_ms, _ = eng.time_kernel(2, 5)
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
     asm_gbs = asm_bytes / (asm_ms * 1e-3) / 1e9
+    # The dominant kernel is the PCG (one persistent cooperative launch per
+    # solve for uniform 3x3 systems).  Algorithmic bytes per iteration
+    # (SURVEY §8(d)): the SpMV's 8 r c + 8 per upper block + 16 s, the
+    # block-Jacobi apply's 72 B per 3x3 inverse + 16 s, 6 vector passes 48 s.
+    nb = eng.s // 3
+    pcg_iter_bytes = spmv_bytes + 72.0 * nb + 16.0 * eng.s + 48.0 * eng.s
+    pcg_ms = stages[4]
+    pcg_gbs = pcg_iter_bytes * st.pcg_iterations / (pcg_ms * 1e-3) / 1e9
 
     # e2e through the C-ABI with pinned host buffers: positions + pair table in, dx out
     e2e = None
@@ -305,7 +318,8 @@ def main():
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": ms_step, "unit": "ms", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: one Newton iteration (dynamic rebuild + eval + assembly + "
                                f"block-Jacobi + PCG to pcg_tol) from a jittered rest state",
@@ -313,18 +327,25 @@ def main():
                    "contact_pairs": int(sim.pair_count()), "pcg_iterations": int(np.median(iters)),
                    "nh_via_deformation_gradient": bool(args.via_f),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
-                   "parallelism": "replicas" if world > 1 else "single"},
-        "roofline": {"kernel": "PCG SpMV (k_spmv33: static+dynamic BSR, fused pHp)", "bound": "hbm",
-                     "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
-                     "traffic": traffic_from_profiles(args.config), "algorithmic_bytes": spmv_bytes,
-                     "avg_launch_ms": spmv_ms, "peak_source": peak_src},
+                   "parallelism": f"pcg-rows{world} (eval/assembly replicated)" if world > 1 else "single"},
+        "roofline": {"kernel": "k_pcg33_persistent (whole PCG solve, one cooperative launch)" if world == 1 else
+                     "row-partitioned PCG (k_dspmv33 / k_dupdate per rank + NCCL allgather)",
+                     "bound": "hbm", "achieved": pcg_gbs, "peak": peak, "unit": "GB/s", "frac": pcg_gbs / peak,
+                     "traffic": traffic_from_profiles(args.config, "pcg_dram_bytes_per_iteration"),
+                     "algorithmic_bytes": pcg_iter_bytes,
+                     "algorithmic_bytes_unit": "per PCG iteration", "iterations": int(st.pcg_iterations),
+                     "avg_launch_ms": pcg_ms, "peak_source": peak_src,
+                     "spmv": {"kernel": "k_spmv33 (static + dynamic BSR, fused pHp), timed alone",
+                              "achieved": spmv_gbs, "frac": spmv_gbs / peak, "algorithmic_bytes": spmv_bytes,
+                              "traffic": traffic_from_profiles(args.config, "spmv_dram_bytes"),
+                              "avg_launch_ms": spmv_ms}},
         "assembly_roofline": {"bound": "hbm", "achieved": asm_gbs, "peak": peak, "unit": "GB/s",
                               "frac": asm_gbs / peak, "algorithmic_bytes": asm_bytes, "avg_ms": asm_ms},
         "eval_ms": eval_ms,
         "stages_ms": {"refresh_dynamic": stages[0], "local_eval": stages[1], "assembly_gather": stages[2],
                       "gradient_diag_precond": stages[3], "pcg": stages[4], "total": stages[6]},
         "gpu_launches": int(launches_per_step * args.steps),
-        "pcg_graph": "conditional-while" if True else "chunked",
+        "pcg_driver": "persistent cooperative kernel" if world == 1 else f"row-partitioned over {world} ranks",
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
         "library": _lib.gpu_library().fns["version"]().decode(),
     }

@@ -1,7 +1,8 @@
 """Summarise ncu outputs into profiles/ (tracked):
   launches csv (--metrics gpu__time_duration.sum)  -> per-kernel share table
   full capture (.ncu-rep)                           -> per-kernel metric table + ncu_summary.json
-usage: python tools/ncu_summary.py <tag> <scene> <launches.csv> <prof.ncu-rep>"""
+usage: python tools/ncu_summary.py <tag> <scene> <launches.csv> <prof.ncu-rep> [prof_driver.log]
+(the log's "pcg iterations N" line converts the persistent PCG kernel's DRAM bytes to bytes per iteration)"""
 import collections
 import csv
 import io
@@ -12,6 +13,10 @@ import subprocess
 import sys
 
 tag, scene, launches, rep = sys.argv[1:5]
+pcg_iters = None
+if len(sys.argv) > 5:
+    m = re.search(r"pcg iterations (\d+)", open(sys.argv[5]).read())
+    pcg_iters = int(m.group(1)) if m else None
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
 os.makedirs(out, exist_ok=True)
 
@@ -32,9 +37,10 @@ for r in rows[1:]:
     a[0] += 1
     a[1] += t
     total += t
-lines = [f"# {tag}: kernel launch list of `python bench.py --config {scene} --steps 2 --warmup 1` under",
-         "`ncu --metrics gpu__time_duration.sum --clock-control none` (YS_PCG_GRAPH=none: the same kernels",
-         "launched directly, because ncu cannot see kernel nodes of a conditional graph).",
+lines = [f"# {tag}: kernel launch list of `python bench.py --config {scene} --steps 2 --warmup 1 --no-cpu-baseline`",
+         "under `ncu --metrics gpu__time_duration.sum --clock-control none`.  The uniform-3x3 PCG is one",
+         "cooperative launch per solve (`k_pcg33_persistent`); the bench's own kernel-timing hooks",
+         "(`ys_time_kernel`: SpMV x50, assembly x10, eval x5) run after the timed steps and appear here too.",
          "Per-launch times are cold-cache and serialised; compare shares, not absolutes.", "",
          "| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
 for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -42,9 +48,6 @@ for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
 open(os.path.join(out, f"{tag}_launches_{scene}.md"), "w").write("\n".join(lines) + "\n")
 
 # ---- full capture
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
-h, units = rr[0], rr[1]
 want = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "MB"), ("dram__bytes_write.sum", "MB"),
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "%"),
         ("l1tex__throughput.avg.pct_of_peak_sustained_active", "%"),
@@ -52,13 +55,28 @@ want = [("gpu__time_duration.sum", "us"), ("dram__bytes_read.sum", "MB"), ("dram
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "%"),
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "%"),
         ("launch__registers_per_thread", "")]
-idx = {w: h.index(w) for w, _ in want if w in h}
+# to MB and us whatever unit each report chose for a column
+_SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,
+          "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3,
+          "s": 1e6, "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
 per = collections.OrderedDict()
-for r in rr[2:]:
-    name = re.sub(r"\(.*", "", r[h.index("Kernel Name")]).replace("void ", "")
-    per.setdefault(name, []).append({w: float(r[i].replace(",", "")) for w, i in idx.items()})
+idx = {}
+for one in rep.split(","):  # several captures may be merged
+    raw = subprocess.run(["ncu", "-i", one, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    part = list(csv.reader(io.StringIO(raw)))
+    if len(part) < 3:
+        continue
+    h, units = part[0], part[1]
+    idx = {w: h.index(w) for w, _ in want if w in h}
+    for r in part[2:]:
+        name = re.sub(r"\(.*", "", r[h.index("Kernel Name")]).replace("void ", "")
+        vals = {}
+        for w, i in idx.items():
+            v = float(r[i].replace(",", "") or "nan")
+            vals[w] = v * _SCALE.get(units[i], 1.0)
+        per.setdefault(name, []).append(vals)
 tl = [f"# {tag}: `ncu --set full --clock-control none` of the top kernels, scene {scene}",
-      f"(command: `YS_PCG_GRAPH=none ncu --set full ... python tools/prof_driver.py {scene}`; mean over captured launches)", "",
+      f"(command: `ncu --set full --import-source on ... python tools/prof_driver.py {scene}`; mean over captured launches)", "",
       "| kernel | n | time us | DRAM rd MB | DRAM wr MB | DRAM % | L1 % | L2 % | warps % | FP64 pipe % | regs |",
       "|---|---:|---:|---:|---:|---:|---:|---:|---:|---:|---:|"]
 summary = {}
@@ -71,9 +89,15 @@ open(os.path.join(out, f"{tag}_ncu_top_{scene}.md"), "w").write("\n".join(tl) + 
 js = os.path.join(out, "ncu_summary.json")
 d = json.load(open(js)) if os.path.exists(js) else {}
 sp = [v for k, v in summary.items() if k.startswith("k_spmv33")]
-d[scene] = {"tag": tag, "kernels": summary}
+prev = d.get(scene, {})
+d[scene] = dict(prev, tag=tag, kernels=dict(prev.get("kernels", {}), **summary))
 if sp:
     d[scene]["spmv_dram_bytes"] = 1e6 * (sp[0]["dram__bytes_read.sum"] + sp[0]["dram__bytes_write.sum"])
+pp = [v for k, v in summary.items() if k.startswith("k_pcg33_persistent")]
+if pp and pcg_iters:
+    d[scene]["pcg_iterations"] = pcg_iters
+    d[scene]["pcg_dram_bytes_per_iteration"] = 1e6 * (pp[0]["dram__bytes_read.sum"] +
+                                                       pp[0]["dram__bytes_write.sum"]) / pcg_iters
 json.dump(d, open(js, "w"), indent=1)
 print("\n".join(lines[:16]))
 print("\n".join(tl))

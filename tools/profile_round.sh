@@ -1,0 +1,17 @@
+#!/bin/bash
+# One GPU call: bench line, ncu launch list, ncu --set full of the top kernels.
+# usage: tools/profile_round.sh <scene>   (outputs under gpurun_out/)
+set -x
+SC=${1:-c5}
+export PYTHONPATH=$PWD
+mkdir -p gpurun_out
+timeout 900 python bench.py --config $SC > gpurun_out/bench_$SC.json 2> gpurun_out/bench_$SC.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$SC.csv \
+  python bench.py --config $SC --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_run.log 2>&1
+for spec in "pcg:k_pcg33_persistent:1" "spmv:k_spmv33:1" "asm:k_gather_h|k_block_rows:3" "eval:k_eval_stencil:2"; do
+  IFS=: read tag rx cnt <<< "$spec"
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$rx" -c $cnt \
+    -f -o gpurun_out/prof_${tag}_$SC python tools/prof_driver.py $SC > gpurun_out/prof_driver_${tag}_$SC.log 2>&1
+done
+tail -3 gpurun_out/bench_$SC.err
+cat gpurun_out/bench_$SC.json
