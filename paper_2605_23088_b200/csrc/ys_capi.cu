@@ -84,39 +84,6 @@ __global__ void k_step(int64_t s, const double* X0, const double* DX, double alp
   if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
 }
 
-// Proximity filter of refresh_dynamic_pairs: d2 = |p_a - p_b|^2 evaluated as
-// ((dx*dx + dy*dy) + dz*dz) with explicit rounding (no FMA) like the CPU.
-__device__ __forceinline__ bool close_pair(const double* a, const double* b, double dhat) {
-  const double dx = __dsub_rn(a[0], b[0]);
-  const double dy = __dsub_rn(a[1], b[1]);
-  const double dz = __dsub_rn(a[2], b[2]);
-  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  return d2 < dhat;
-}
-
-__global__ void k_pair_count(const double* pa, int64_t na, const double* pb, int64_t nb, double dhat, int32_t* cnt) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= na) return;
-  const double p[3] = {pa[3 * i], pa[3 * i + 1], pa[3 * i + 2]};
-  int32_t c = 0;
-  for (int64_t j = 0; j < nb; ++j) c += close_pair(p, pb + 3 * j, dhat) ? 1 : 0;
-  cnt[i] = c;
-}
-
-__global__ void k_pair_emit(const double* pa, int64_t na, const double* pb, int64_t nb, double dhat,
-                            const int32_t* off, int64_t base_a, int64_t base_b, int32_t* out) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= na) return;
-  const double p[3] = {pa[3 * i], pa[3 * i + 1], pa[3 * i + 2]};
-  int64_t w = off[i];
-  for (int64_t j = 0; j < nb; ++j)
-    if (close_pair(p, pb + 3 * j, dhat)) {
-      out[2 * w] = int32_t(base_a + i);
-      out[2 * w + 1] = int32_t(base_b + j);
-      ++w;
-    }
-}
-
 __global__ void k_identity_minv(int64_t nb, int bs, double* minv, int32_t* flag) {
   const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= nb) return;
@@ -268,60 +235,11 @@ void ctx_get_points(Context& c, int domain, double* out) {
   YS_CUDA(cudaStreamSynchronize(c.stream));
 }
 
-void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed, int64_t* n_pairs) {
-  PairSet& ps = c.pairsets[pairset];
-  Union& u = c.unions[ps.uni];
-  cudaStream_t s = c.stream;
-  const int nc = int(u.children.size());
-  std::vector<DevBuf<double>> pos(nc);
-  std::vector<int64_t> base(nc);
-  int64_t acc = 0;
-  for (int k = 0; k < nc; ++k) {
-    Domain& d = c.domains[u.children[k]];
-    base[k] = acc;
-    acc += d.n;
-    pos[k].resize(size_t(3 * std::max<int64_t>(d.n, 1)));
-    if (d.n) k_points<<<grid_for(d.n), kTB, 0, s>>>(domain_dev(c, d), c.X.p, pos[k].p);
-  }
-  std::vector<int32_t> all;
-  DevBuf<int32_t> cnt, off, out;
-  for (int ca = 0; ca < nc; ++ca)
-    for (int cb = ca + 1; cb < nc; ++cb) {
-      const bool fa = child_fixed ? child_fixed[ca] != 0 : c.domains[u.children[ca]].kind == YS_POINTS_FIXED;
-      const bool fb = child_fixed ? child_fixed[cb] != 0 : c.domains[u.children[cb]].kind == YS_POINTS_FIXED;
-      if (fa && fb) continue;
-      const int64_t na = c.domains[u.children[ca]].n, nbb = c.domains[u.children[cb]].n;
-      if (na == 0 || nbb == 0) continue;
-      cnt.resize(na);
-      off.resize(na);
-      k_pair_count<<<grid_for(na, 128), 128, 0, s>>>(pos[ca].p, na, pos[cb].p, nbb, dhat, cnt.p);
-      YS_LAUNCH_CHECK();
-      size_t bytes = 0;
-      int32_t* ci = cnt.p;
-      int32_t* co = off.p;
-      const int nai = int(na);
-      YS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, ci, co, nai, s));
-      c.cubtmp.resize(std::max<size_t>(bytes, 1));
-      YS_CUDA(cub::DeviceScan::ExclusiveSum(c.cubtmp.p, bytes, ci, co, nai, s));
-      int32_t last_off = 0, last_cnt = 0;
-      YS_CUDA(cudaMemcpyAsync(&last_off, co + na - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      YS_CUDA(cudaMemcpyAsync(&last_cnt, ci + na - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      YS_CUDA(cudaStreamSynchronize(s));
-      const int64_t tot = int64_t(last_off) + last_cnt;
-      if (tot == 0) continue;
-      out.resize(size_t(2 * tot));
-      k_pair_emit<<<grid_for(na, 128), 128, 0, s>>>(pos[ca].p, na, pos[cb].p, nbb, dhat, co, base[ca], base[cb],
-                                                     out.p);
-      YS_LAUNCH_CHECK();
-      std::vector<int32_t> h = out.to_host(s);
-      all.insert(all.end(), h.begin(), h.end());
-    }
-  ps.n = int64_t(all.size() / 2);
-  ps.h_pairs.assign(all.begin(), all.end());
-  ps.pairs.upload(all, s);
-  ++c.epoch;
-  if (n_pairs) *n_pairs = ps.n;
-  YS_CUDA(cudaStreamSynchronize(s));
+void ctx_domain_points(Context& c, int domain, double* out) {
+  const Domain& d = c.domains[domain];
+  if (d.n == 0) return;
+  k_points<<<grid_for(d.n), kTB, 0, c.stream>>>(domain_dev(c, d), c.X.p, out);
+  YS_LAUNCH_CHECK();
 }
 
 }  // namespace ys
@@ -564,6 +482,7 @@ int ys_set_pairs(ys_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
     check_pairs_in_range(*c, p, n, pairs);
     p.n = n;
     p.h_pairs.assign(pairs, pairs + 2 * n);
+    p.host_stale = false;
     if (c->finalized) {
       std::vector<int32_t> q(pairs, pairs + 2 * n);
       p.pairs.upload(q, c->stream);
@@ -583,7 +502,12 @@ int ys_pair_count(ys_context* c, int32_t ps, int64_t* n) {
 int ys_get_pairs(ys_context* c, int32_t ps, int64_t* out) {
   return guarded(c, [&] {
     if (ps < 0 || ps >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown pair set");
-    const PairSet& p = c->pairsets[ps];
+    PairSet& p = c->pairsets[ps];
+    if (p.host_stale) {
+      std::vector<int32_t> h = p.pairs.to_host(c->stream);
+      p.h_pairs.assign(h.begin(), h.begin() + 2 * p.n);
+      p.host_stale = false;
+    }
     std::copy(p.h_pairs.begin(), p.h_pairs.end(), out);
   });
 }

@@ -59,7 +59,17 @@ struct PairSet {
   bool dynamic = false;
   int64_t n = 0;
   std::vector<int64_t> h_pairs;
+  bool host_stale = false;  // set by the device refresh; get_pairs downloads lazily
   DevBuf<int32_t> pairs;  // 2n union-global indices
+};
+
+// Device scratch of the contact-candidate refresh (ys_contact.cu), reused.
+struct ContactScratch {
+  DevBuf<double> pos;              // 3 x union size, union order
+  DevBuf<double> part, boxes;
+  DevBuf<uint64_t> keys, keys_out;  // per-child slices (B side of a child pair)
+  DevBuf<int32_t> idx, idx_out;
+  DevBuf<int32_t> cnt, off, scratch;
 };
 
 // A compiled energy term group (CompiledEnergy, assembly.hpp:75-103).
@@ -227,6 +237,7 @@ struct Context {
   cudaEvent_t ev[10] = {};
 
   DistState dist;
+  ContactScratch contact;
 
   // free-standing BSR systems (ys_bsr_*)
   struct Bsr {

@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 
 from paper_2605_23088_b200 import NumericalError, ValidationError
-from paper_2605_23088_b200.engine import YS_PROJECT_FULL, YS_PROJECT_REDUCED, BlockSystem, Engine
+from paper_2605_23088_b200.engine import (YS_POINTS_AFFINE, YS_POINTS_FIXED, YS_POINTS_FREE, YS_PROJECT_FULL,
+                                          YS_PROJECT_REDUCED, BlockSystem, Engine)
 from fixtures import ContactScene, random_system, rel, tet_scene
 
 pytestmark = pytest.mark.gpu
@@ -251,3 +252,45 @@ def test_newton_frames_positions():
         po = np.concatenate([p.ravel() for p in sims[1].positions()])
         assert rel(pg, po) <= TOL
         assert sims[0].pair_count() == sims[1].pair_count()
+
+
+@pytest.mark.parametrize("dhat", [0.0, 0.01, 0.0625, 0.5])
+def test_contact_candidates_grid_bit_exact(dhat):
+    """The device grid candidates (ys_contact.cu) against the oracle's
+    all-pairs loop (sim.cpp:456-484): identical pair list and order.  Dense
+    clouds, coordinates on multiples of sqrt(dhat) (cell boundaries), pairs at
+    exactly d2 == dhat (excluded), a fixed child (fixed-fixed skipped)."""
+    rng = np.random.default_rng(5)
+    h = np.sqrt(dhat) if dhat > 0 else 0.1
+
+    def build(eng):
+        n_free, n_bodies, n_abd, n_fix = 400, 3, 300, 200
+        free = rng.uniform(-0.6, 0.6, (n_free, 3)) if eng.backend == "gpu" else build.free
+        build.free = free
+        free[:40] = np.round(free[:40] / h) * h  # on cell boundaries
+        free[40] = free[41] + np.array([h, 0.0, 0.0])  # d2 == dhat exactly (not a pair)
+        t_free = eng.add_target(n_free, 3, free)
+        av = np.tile(np.eye(3).reshape(-1), (n_bodies, 1))
+        t_A = eng.add_target(n_bodies, 9, av)
+        t_t = eng.add_target(n_bodies, 3, np.zeros((n_bodies, 3)))
+        rest = build.rest if hasattr(build, "rest") else rng.uniform(-0.5, 0.5, (n_abd, 3))
+        build.rest = rest
+        fix = build.fix if hasattr(build, "fix") else rng.uniform(-0.7, 0.7, (n_fix, 3))
+        build.fix = fix
+        d_free = eng.add_points(YS_POINTS_FREE, n_free, t_free)
+        d_abd = eng.add_points(YS_POINTS_AFFINE, n_abd, t_A, t_t,
+                               np.array([i * n_bodies // n_abd for i in range(n_abd)], dtype=np.int64), rest)
+        d_fix = eng.add_points(YS_POINTS_FIXED, n_fix, rest=fix)
+        d_fix2 = eng.add_points(YS_POINTS_FIXED, 50, rest=fix[:50] + 1e-3)
+        uni = eng.add_point_union([d_free, d_abd, d_fix, d_fix2])
+        pp = eng.add_pair_set(uni, True)
+        eng.add_point_point_barrier(pp, max(dhat, 1e-3), 1.0, 1.0)
+        return pp
+
+    (g, pg), (o, po) = both(build)
+    flags = [0, 0, 1, 1]
+    ng, no = g.refresh_pairs(pg, dhat, flags), o.refresh_pairs(po, dhat, flags)
+    assert ng == no
+    assert np.array_equal(g.get_pairs(pg), o.get_pairs(po))
+    if dhat >= 0.01:
+        assert ng > 0
