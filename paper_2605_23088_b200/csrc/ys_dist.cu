@@ -185,7 +185,7 @@ __global__ void k_copy_rows(const double* __restrict__ x, int64_t r0, int64_t r1
 // ---------------------------------------------------------------------------
 // Solver kernels over the owned rows [r0, r1); rank partials -> out.
 
-__global__ void __launch_bounds__(kTB, 4) k_dspmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1,
+__global__ void __launch_bounds__(kTB, kSpmvMinB) k_dspmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1,
                                                     const double* __restrict__ x, double* __restrict__ y,
                                                     PcgState* st, double* part, double* out) {
   constexpr int SW = kSpmvSW;
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kTB, 4) k_dspmv33(SpmvDev S0, SpmvDev S1, int 
     RowPtrs p1{0, 0, 0, 0};
     if (has1) p1 = load_rowptrs(S1, R);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33<SW>(S0, p0, lane, x, a0, a1, a2);
-    if (has1) acc33<SW>(S1, p1, lane, x, a0, a1, a2);
+    acc33_u2<SW>(S0, p0, lane, x, a0, a1, a2);
+    if (has1) acc33_u2<SW>(S1, p1, lane, x, a0, a1, a2);
 #pragma unroll
     for (int off = SW / 2; off > 0; off >>= 1) {
       a0 += __shfl_xor_sync(mask, a0, off, SW);

@@ -29,7 +29,7 @@ namespace ys {
 
 // y(+)= (S0 + S1) x over uniform 3-DoF block rows; optional p.y partials
 // reduced to pHp and alpha by the last CTA.
-__global__ void __launch_bounds__(kTB, 4) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+__global__ void __launch_bounds__(kTB, kSpmvMinB) k_spmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
                                                    const double* __restrict__ x, double* __restrict__ y,
                                                    int accumulate, PcgState* st, double* part) {
   constexpr int SW = kSpmvSW;
@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(kTB, 4) k_spmv33(SpmvDev S0, SpmvDev S1, int h
     RowPtrs p1{0, 0, 0, 0};
     if (has1) p1 = load_rowptrs(S1, R);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33<SW>(S0, p0, lane, x, a0, a1, a2);
-    if (has1) acc33<SW>(S1, p1, lane, x, a0, a1, a2);
+    acc33_u2<SW>(S0, p0, lane, x, a0, a1, a2);
+    if (has1) acc33_u2<SW>(S1, p1, lane, x, a0, a1, a2);
 #pragma unroll
     for (int off = SW / 2; off > 0; off >>= 1) {
       a0 += __shfl_xor_sync(mask, a0, off, SW);
@@ -144,6 +144,44 @@ __global__ void __launch_bounds__(kTB, MINB) k_spmv33_var(SpmvDev S0, int64_t nb
   }
 }
 
+template <int SW, int MINB>
+__global__ void __launch_bounds__(kTB, MINB) k_spmv33_u2(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x % SW;
+  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
+  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
+  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
+  for (int64_t R = sw0; R < nb; R += nsw) {
+    const RowPtrs p0 = load_rowptrs(S0, R);
+    RowPtrs p1{0, 0, 0, 0};
+    if (has1) p1 = load_rowptrs(S1, R);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    acc33_u2<SW>(S0, p0, lane, x, a0, a1, a2);
+    if (has1) acc33_u2<SW>(S1, p1, lane, x, a0, a1, a2);
+#pragma unroll
+    for (int off = SW / 2; off > 0; off >>= 1) {
+      a0 += __shfl_xor_sync(mask, a0, off, SW);
+      a1 += __shfl_xor_sync(mask, a1, off, SW);
+      a2 += __shfl_xor_sync(mask, a2, off, SW);
+    }
+    if (lane == 0) {
+      y[3 * R] = a0;
+      y[3 * R + 1] = a1;
+      y[3 * R + 2] = a2;
+    }
+  }
+}
+
+template <class K>
+static void launch_u2(Context& c, K kern, const double* x, double* y) {
+  int occ = 0;
+  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+  const bool has1 = c.S[1].n_blocks > 0;
+  SpmvDev d0 = spmv_dev(c.S[0]), d1 = spmv_dev(c.S[has1 ? 1 : 0]);
+  kern<<<std::max(1, occ) * sm_count(), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y);
+  YS_LAUNCH_CHECK();
+}
+
 template <class K>
 static void launch_var(Context& c, K kern, SpmvDev d0, const double* x, double* y) {
   int occ = 0;
@@ -167,6 +205,12 @@ bool spmv_variant(Context& c, int v, const double* x, double* y) {
     case 10: launch_var(c, k_spmv33_var<16, 4, 0, false>, d0, x, y); return true;
     case 11: launch_var(c, k_spmv33_var<4, 5, 0, true>, d0, x, y); return true;
     case 12: launch_var(c, k_spmv33_var<2, 4, 0, true>, d0, x, y); return true;
+    // static + dynamic, two entries per lane per trip (13: one entry per trip, the pre-u2 kernel)
+    case 13: launch_u2(c, k_spmv33_u2<4, 4>, x, y); return true;
+    case 14: launch_u2(c, k_spmv33_u2<4, 3>, x, y); return true;
+    case 15: launch_u2(c, k_spmv33_u2<8, 3>, x, y); return true;
+    case 16: launch_u2(c, k_spmv33_u2<2, 3>, x, y); return true;
+    case 17: launch_u2(c, k_spmv33_u2<4, 2>, x, y); return true;
   }
   return false;
 }
@@ -461,7 +505,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__global__ void __launch_bounds__(kTB, 4) k_pcg33_persistent(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+template <int TB, int MINB>
+__global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
                                                              const double* __restrict__ minv, double* __restrict__ x,
                                                              double* __restrict__ r, double* __restrict__ z,
                                                              double* __restrict__ p, double* __restrict__ hp,
@@ -490,8 +535,8 @@ __global__ void __launch_bounds__(kTB, 4) k_pcg33_persistent(SpmvDev S0, SpmvDev
       RowPtrs p1{0, 0, 0, 0};
       if (has1) p1 = load_rowptrs(S1, R);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      acc33<SW>(S0, p0, lane, p, a0, a1, a2);
-      if (has1) acc33<SW>(S1, p1, lane, p, a0, a1, a2);
+      acc33_u2<SW>(S0, p0, lane, p, a0, a1, a2);
+      if (has1) acc33_u2<SW>(S1, p1, lane, p, a0, a1, a2);
 #pragma unroll
       for (int off = SW / 2; off > 0; off >>= 1) {
         a0 += __shfl_xor_sync(mask, a0, off, SW);
@@ -776,11 +821,11 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
     const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
     static const bool persistent_off = getenv("YS_PCG_PERSISTENT") && std::string(getenv("YS_PCG_PERSISTENT")) == "0";
     if (fast && !persistent_off) {
-      static int occ = 0;
-      if (!occ) {
-        YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg33_persistent, kTB, 0));
-        if (occ < 1) occ = 1;
-      }
+      // 256 x 3 CTAs per SM (384 x 2, the same 768 threads, measured equal at C5)
+      void* kern = reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB>);
+      int occ = 0;
+      YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+      if (occ < 1) occ = 1;
       int gsz = occ * sm_count();
       c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
       c.gridbar.resize(sizeof(GridBar));
@@ -795,8 +840,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       PcgState* stp = c.pcg.p;
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
       void* args[] = {&d0, &d1, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
-      YS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg33_persistent), dim3(gsz), dim3(kTB), args, 0,
-                                          s));
+      YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
       PcgState fin{};
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
