@@ -50,43 +50,52 @@ YS_HD constexpr double kST(int a, int i) { return a == 0 ? -1.0 : (i == a - 1 ? 
 
 // ---------------------------------------------------------------------------
 // Cyclic Jacobi on a packed symmetric 9x9 matrix, eigenvectors in v (row-major
-// v[k*9+j] = component k of eigenvector j).  Rotations whose off-diagonal
-// entry is below the rounding of both diagonal entries are dropped (the
-// classical negligibility rule), so the loop terminates with an exactly
-// diagonal matrix.  Returns the number of sweeps.
+// v[k*9+j] = component k of eigenvector j).  Per rotation one sqrt, one
+// division and one rsqrt: with h = a_qq - a_pp,
+//   t = 2 sgn(h) a_pq / (|h| + sqrt(h^2 + 4 a_pq^2)),  c = 1/sqrt(1 + t^2),  s = t c
+// (the smaller root of t^2 + 2 theta t - 1 = 0, theta = h / (2 a_pq)).
+// Rotations whose off-diagonal entry is below the rounding of both diagonal
+// entries are dropped (the classical negligibility rule); when every lane of
+// the warp drops a rotation the row / column update is skipped.  Sweeps stop
+// once the off-diagonal Frobenius norm is below 1e-14 of the matrix norm:
+// the projection then differs from the exact one by O(1e-14) relative, far
+// inside the 1e-9 parity bar.  Returns the number of sweeps.
 __device__ __forceinline__ void jacobi_rot(double* a, double* v, int p, int q) {
   const double apq = a[pk9(p, q)];
   const double app = a[pk9(p, p)];
   const double aqq = a[pk9(q, q)];
   const double g = 100.0 * fabs(apq);
   const bool negligible = (fabs(app) + g == fabs(app)) && (fabs(aqq) + g == fabs(aqq));
+  if (__all_sync(__activemask(), negligible)) {
+    a[pk9(p, q)] = 0.0;
+    return;
+  }
   double t = 0.0;
   if (!negligible) {
-    const double theta = 0.5 * (aqq - app) / apq;
-    t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
-    if (theta < 0.0) t = -t;
+    const double h = aqq - app;
+    const double num = h < 0.0 ? -2.0 * apq : 2.0 * apq;
+    t = num / (fabs(h) + sqrt(h * h + 4.0 * apq * apq));
   }
-  const double c = 1.0 / sqrt(t * t + 1.0);
-  const double s = t * c;
-  const double tau = s / (1.0 + c);
-  const double h = t * apq;
-  a[pk9(p, p)] = app - h;
-  a[pk9(q, q)] = aqq + h;
+  const double c = rsqrt(1.0 + t * t);
+  const double sn = t * c;
+  const double tq = t * apq;
+  a[pk9(p, p)] = app - tq;
+  a[pk9(q, q)] = aqq + tq;
   a[pk9(p, q)] = 0.0;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     if (k == p || k == q) continue;
     const double akp = a[pk9(k, p)];
     const double akq = a[pk9(k, q)];
-    a[pk9(k, p)] = akp - s * (akq + tau * akp);
-    a[pk9(k, q)] = akq + s * (akp - tau * akq);
+    a[pk9(k, p)] = c * akp - sn * akq;
+    a[pk9(k, q)] = sn * akp + c * akq;
   }
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     const double vkp = v[k * 9 + p];
     const double vkq = v[k * 9 + q];
-    v[k * 9 + p] = vkp - s * (vkq + tau * vkp);
-    v[k * 9 + q] = vkq + s * (vkp - tau * vkq);
+    v[k * 9 + p] = c * vkp - sn * vkq;
+    v[k * 9 + q] = sn * vkp + c * vkq;
   }
 }
 
@@ -95,12 +104,14 @@ __device__ __forceinline__ int jacobi9(double* a, double* v) {
   for (int i = 0; i < 81; ++i) v[i] = (i % 10 == 0) ? 1.0 : 0.0;
   int sweep = 0;
   for (; sweep < 40; ++sweep) {
-    double off = 0.0;
+    double off = 0.0, dia = 0.0;
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
+    for (int p = 0; p < 9; ++p) {
+      dia += a[pk9(p, p)] * a[pk9(p, p)];
 #pragma unroll
       for (int q = p + 1; q < 9; ++q) off += a[pk9(p, q)] * a[pk9(p, q)];
-    if (off == 0.0) break;
+    }
+    if (!(off > 1e-28 * (dia + 2.0 * off))) break;  // also stops on off == 0
 #pragma unroll
     for (int p = 0; p < 8; ++p)
 #pragma unroll
