@@ -52,6 +52,7 @@ int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
 void ctx_gather_all(Context& c);
 bool spmv_variant(Context& c, int v, const double* x, double* y);
+void barrier_probe(Context& c, int n, int with_reduce);
 
 void ctx_eval_all(Context& c, bool project, bool with_hessian);
 
@@ -1143,7 +1144,9 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
     cudaStream_t s = c->stream;
     double alg = 0.0;
     auto launch = [&]() {
-      if (which >= 10) {
+      if (which == 5 || which == 6) {  // 1000 counter grid barriers per launch (6: + partial reductions)
+        barrier_probe(*c, 1000, which == 6 ? 3 : 2);
+      } else if (which >= 10) {
         if (!spmv_variant(*c, which - 10, c->p.p, c->hp.p)) fail(YS_ERR_VALIDATION, "unknown SpMV variant");
       } else if (which == 0) {
         spmv_launch(*c, c->S[0], &c->S[1], c->p.p, c->hp.p, false, nullptr, nullptr, pcg_grid(*c));

@@ -458,8 +458,9 @@ __global__ void k_pupdate(int64_t s, const double* __restrict__ z, double* __res
 // per-CTA partials in the same fixed order, so all CTAs hold bit-identical
 // alpha / beta / status without a last-CTA round trip (deterministic).
 struct GridBar {
-  unsigned int count;
+  unsigned int count;  // generation barrier
   unsigned int gen;
+  unsigned long long arrivals;  // counter barrier: only grows within a launch
 };
 
 __device__ __forceinline__ void grid_sync(GridBar* gb) {
@@ -476,6 +477,26 @@ __device__ __forceinline__ void grid_sync(GridBar* gb) {
       while (*vgen == g) __nanosleep(20);
     }
     __threadfence();
+  }
+  __syncthreads();
+}
+
+// Counter barrier: one red.release (no return value) per CTA on a counter
+// that only grows, then acquire-polling until it reaches G * epoch.  The
+// release orders this CTA's writes before its arrival; the acquire load orders
+// the poller's later reads after every arrival (and invalidates L1).  No
+// returning atomic is serialised at one address and no generation word is
+// needed; the counter is zeroed before each launch.
+__device__ __forceinline__ void grid_sync_counter(unsigned long long* count, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
   }
   __syncthreads();
 }
@@ -526,6 +547,7 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
   long long it = 0;
   double rel = st->rel, php = 0.0, alpha = 0.0;
   unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long epoch = 0;  // grid barriers passed (the counter is zeroed before the launch)
   unsigned long long t0 = gtimer();
   while (status == 0) {
     // ---- phase A: hp = H p, pHp partials
@@ -553,7 +575,7 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
     }
     block_reduce<1>(dot);
     if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
-    grid_sync(gb);
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
     unsigned long long t1 = gtimer();
     ph[0] += t1 - t0;
     t0 = t1;
@@ -595,7 +617,7 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
       part[G + blockIdx.x] = v[0];
       part[2 * G + blockIdx.x] = v[1];
     }
-    grid_sync(gb);
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
     t1 = gtimer();
     ph[1] += t1 - t0;
     t0 = t1;
@@ -635,7 +657,7 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
       }
       if (((3 * nb) & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[3 * nb - 1] = z[3 * nb - 1] + beta * p[3 * nb - 1];
     }
-    grid_sync(gb);
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
     t1 = gtimer();
     ph[3] += t1 - t0;
     t0 = t1;
@@ -701,6 +723,46 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
     k_dot_alpha<<<grid, kTB, 0, c.stream>>>(c.s, x, y, st, part);
     YS_LAUNCH_CHECK();
   }
+}
+
+// Diagnostic: n grid barriers (and n fixed-order partial reductions) at the
+// persistent PCG's grid, to price the per-iteration synchronisation.  Bit 1:
+// counter barrier (production) instead of the generation barrier; bit 0: +
+// reduce_partials_all.  Measured on B200 at 444 CTAs: generation barrier
+// 3.1 us, counter barrier 2.2 us, + reduction ~1.1 us.  Also measured and
+// dropped: 32 striped counters 3.5 us, relaxed polling 2.3 us, 256 ns backoff
+// 2.6 us, master release through per-CTA flag lines 4.3 us.
+__global__ void __launch_bounds__(kTB, kSpmvMinB) k_barrier_probe(GridBar* gb, int n, int with_reduce, double* part,
+                                                                  double* out) {
+  double acc = 0.0;
+  for (int k = 0; k < n; ++k) {
+    if (with_reduce & 1) {
+      if (threadIdx.x == 0) part[blockIdx.x] = double(k + blockIdx.x);
+    }
+    if (with_reduce & 2) grid_sync_counter(&gb->arrivals, (unsigned long long)gridDim.x * (k + 1));
+    else grid_sync(gb);
+    if (with_reduce & 1) {
+      double t[1];
+      reduce_partials_all<1>(part, gridDim.x, t);
+      acc += t[0];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = acc;
+}
+
+void barrier_probe(Context& c, int n, int with_reduce) {
+  void* kern = reinterpret_cast<void*>(k_barrier_probe);
+  int occ = 0;
+  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+  int gsz = std::max(1, occ) * sm_count();
+  c.gridbar.resize(sizeof(GridBar));
+  YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), c.stream));
+  c.partials.resize(std::max<size_t>(c.partials.n, size_t(gsz + 1)));
+  GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
+  double* part = c.partials.p;
+  double* out = c.partials.p + gsz;
+  void* args[] = {&gbp, &n, &with_reduce, &part, &out};
+  YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, c.stream));
 }
 
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y) {
