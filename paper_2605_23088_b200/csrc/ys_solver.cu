@@ -23,7 +23,7 @@
 #include <cstdlib>
 #include <chrono>
 
-#include "ys_spmv.cuh"
+#include "ys_sell.cuh"
 
 namespace ys {
 
@@ -526,8 +526,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int TB, int MINB>
-__global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
+// SH = 0: row gather from upper storage (ys_spmv.cuh); SH > 0: the sliced-ELL
+// full copy with SH lanes per block row (ys_sell.cuh).
+template <int TB, int MINB, int SH>
+__global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvDev S1, SellDev SL, int has1, int64_t nb,
                                                              const double* __restrict__ minv, double* __restrict__ x,
                                                              double* __restrict__ r, double* __restrict__ z,
                                                              double* __restrict__ p, double* __restrict__ hp,
@@ -552,7 +554,24 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
   while (status == 0) {
     // ---- phase A: hp = H p, pHp partials
     double dot[1] = {0.0};
-    for (int64_t R = sw0; R < nb; R += nsw) {
+    if constexpr (SH > 0) {
+      const int wl = threadIdx.x & 31;
+      const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+      const int64_t nw = (int64_t(G) * blockDim.x) >> 5;
+      for (int64_t sl = w0; sl < SL.nslices; sl += nw) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        int64_t R;
+        sell_acc<SH>(SL, sl, wl, p, a0, a1, a2, R);
+        if (wl % SH == 0 && R < nb) {
+          double* yo = hp + 3 * R;
+          yo[0] = a0;
+          yo[1] = a1;
+          yo[2] = a2;
+          dot[0] += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
+        }
+      }
+    }
+    for (int64_t R = SH > 0 ? nb : sw0; R < nb; R += nsw) {
       const RowPtrs p0 = load_rowptrs(S0, R);
       RowPtrs p1{0, 0, 0, 0};
       if (has1) p1 = load_rowptrs(S1, R);
@@ -566,6 +585,181 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
         a2 += __shfl_xor_sync(mask, a2, off, SW);
       }
       if (lane == 0) {
+        double* yo = hp + 3 * R;
+        yo[0] = a0;
+        yo[1] = a1;
+        yo[2] = a2;
+        dot[0] += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
+      }
+    }
+    block_reduce<1>(dot);
+    if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    unsigned long long t1 = gtimer();
+    ph[0] += t1 - t0;
+    t0 = t1;
+    double tot1[1];
+    reduce_partials_all<1>(part, G, tot1);
+    php = tot1[0];
+    if (!isfinite(php) || php <= 0.0) {
+      status = php == 0.0 ? 2 : 3;
+      break;
+    }
+    alpha = rz / php;
+    // ---- phase B: x += a p, r -= a hp, z = M^-1 r, partials of r.r and r.z
+    double v[2] = {0.0, 0.0};
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(G) * blockDim.x) {
+      const int64_t s0 = 3 * b;
+      double pp[3], hh[3], rr[3], xx[3], zz[3], M[9];
+      load_vec3(p + s0, pp[0], pp[1], pp[2]);
+      load_vec3_cg(hp + s0, hh[0], hh[1], hh[2]);
+      load_vec3(r + s0, rr[0], rr[1], rr[2]);
+      load_vec3(x + s0, xx[0], xx[1], xx[2]);
+      load_block9(minv + 9 * b, M);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        xx[i] += alpha * pp[i];
+        rr[i] -= alpha * hh[i];
+      }
+      precond_apply<3>(M, rr, zz);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        x[s0 + i] = xx[i];
+        r[s0 + i] = rr[i];
+        z[s0 + i] = zz[i];
+        v[0] += rr[i] * rr[i];
+        v[1] += rr[i] * zz[i];
+      }
+    }
+    block_reduce<2>(v);
+    if (threadIdx.x == 0) {
+      part[G + blockIdx.x] = v[0];
+      part[2 * G + blockIdx.x] = v[1];
+    }
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    t1 = gtimer();
+    ph[1] += t1 - t0;
+    t0 = t1;
+    double tot2[2];
+    reduce_partials_all<2>(part + G, G, tot2);
+    t1 = gtimer();
+    ph[2] += t1 - t0;
+    t0 = t1;
+    rel = sqrt(tot2[0]) / gnorm;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it + 1 < hist_cap) hist[it + 1] = rel;
+    ++it;
+    if (!isfinite(rel)) {
+      status = 4;
+      break;
+    }
+    if (rel <= tol) {
+      status = 1;
+      break;
+    }
+    if (it >= max_iter) {
+      status = 5;
+      break;
+    }
+    const double beta = tot2[1] / rz;
+    rz = tot2[1];
+    // ---- phase C: p = z + beta p
+    {
+      const int64_t n2 = (3 * nb) >> 1;
+      const double2* z2 = reinterpret_cast<const double2*>(z);
+      double2* p2 = reinterpret_cast<double2*>(p);
+      for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(G) * blockDim.x) {
+        const double2 zz = __ldcg(z2 + i);
+        double2 q = p2[i];
+        q.x = zz.x + beta * q.x;
+        q.y = zz.y + beta * q.y;
+        p2[i] = q;
+      }
+      if (((3 * nb) & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[3 * nb - 1] = z[3 * nb - 1] + beta * p[3 * nb - 1];
+    }
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    t1 = gtimer();
+    ph[3] += t1 - t0;
+    t0 = t1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->it += it;
+    st->rel = rel;
+    st->rz = rz;
+    st->php = php;
+    st->alpha = alpha;
+    st->status = status;
+    if (status == 3 || status == 4) st->fail_it = int(it - (status == 4 ? 1 : 0));
+    for (int k = 0; k < 4; ++k) st->phase_ns[k] = ph[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent PCG over the sliced-ELL copy (ys_sell.cuh).
+//
+// Warp w of CTA b owns the slices gw + k * NW (gw = b * 8 + w, k < K) for the
+// whole solve.  Its SpMV plan — each slice's first entry row, each lane's
+// entry count and the column DoFs of all its entries — is loaded into shared
+// memory once, so every SpMV issues the x gathers together with the value
+// stream (no soff -> col -> x dependency chain per slice): C5 phase A 51 ->
+// 45 us.  Phases B and C keep one thread per block row over global vectors
+// (independent loads; a shared-memory row state with the slice mapping was
+// measured slower: its per-row chains are latency-bound).  Fixed-order
+// reductions (deterministic).
+template <int H>
+__global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_sell(SellDev SL, int64_t nb, int K, int TW,
+                                                             const double* __restrict__ minv, double* __restrict__ x,
+                                                             double* __restrict__ r, double* __restrict__ z,
+                                                             double* __restrict__ p, double* __restrict__ hp,
+                                                             PcgState* st, double* part, double* hist, GridBar* gb) {
+  extern __shared__ double smem[];
+  constexpr int RPS = 32 / H;
+  constexpr int WPB = kTB / 32;
+  const int G = gridDim.x;
+  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
+  const int grp = wl / H, h = wl % H;
+  const int64_t gw = int64_t(blockIdx.x) * WPB + warp;
+  const int64_t NW = int64_t(G) * WPB;
+  // plan: per warp K int2 {first entry row, local entry-row offset}, K x 32
+  // lane counts, TW x 32 column DoFs
+  int2* meta = reinterpret_cast<int2*>(smem) + warp * K;
+  int32_t* lhs = reinterpret_cast<int32_t*>(reinterpret_cast<int2*>(smem) + WPB * K) + warp * K * 32;
+  int32_t* cols = lhs + (WPB - warp) * K * 32 + warp * TW * 32;
+  const int kn = gw < SL.nslices ? int(min(int64_t(K), (SL.nslices - gw + NW - 1) / NW)) : 0;
+  {
+    int off = 0;
+    for (int k = 0; k < kn; ++k) {
+      const int64_t sl = gw + k * NW;
+      const int64_t e0 = SL.soff[sl], e1 = SL.soff[sl + 1];
+      const int64_t R = sl * RPS + grp;
+      const int L = R < nb ? SL.len[R] : 0;
+      const int Lh = L > h ? (L - h + H - 1) / H : 0;
+      if (wl == 0) meta[k] = make_int2(int(e0), off);
+      lhs[k * 32 + wl] = Lh;
+      for (int j = 0; j < Lh; ++j) cols[(off + j) * 32 + wl] = SL.col[(e0 + j) * 32 + wl];
+      off += int(e1 - e0);
+    }
+    __syncwarp();
+  }
+  const double gnorm = st->gnorm;
+  const double tol = st->tol;
+  const long long max_iter = st->max_iter;
+  const long long hist_cap = st->hist_cap;
+  double rz = st->rz;
+  int status = st->status;
+  long long it = 0;
+  double rel = st->rel, php = 0.0, alpha = 0.0;
+  unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long epoch = 0;
+  unsigned long long t0 = gtimer();
+  while (status == 0) {
+    // ---- phase A: hp = H p, pHp partials
+    double dot[1] = {0.0};
+    for (int k = 0; k < kn; ++k) {
+      const int2 m = meta[k];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2);
+      const int64_t R = (gw + k * NW) * RPS + grp;
+      if (h == 0 && R < nb) {
         double* yo = hp + 3 * R;
         yo[0] = a0;
         yo[1] = a1;
@@ -883,26 +1077,63 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
     const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
     static const bool persistent_off = getenv("YS_PCG_PERSISTENT") && std::string(getenv("YS_PCG_PERSISTENT")) == "0";
     if (fast && !persistent_off) {
-      // 256 x 3 CTAs per SM (384 x 2, the same 768 threads, measured equal at C5)
-      void* kern = reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB>);
-      int occ = 0;
-      YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
-      if (occ < 1) occ = 1;
-      int gsz = occ * sm_count();
-      c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
-      c.gridbar.resize(sizeof(GridBar));
-      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
-      SpmvDev d0 = spmv_dev(c.S[0]);
-      SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
-      int h1 = has1 ? 1 : 0;
+      // YS_PCG_SELL: lanes per block row of the sliced-ELL copy (0: row gather
+      // from upper storage).
+      static const int sell_h = [] {
+        const char* e = getenv("YS_PCG_SELL");
+        return e ? atoi(e) : 4;
+      }();
+      if (sell_h != 0 && sell_h != 1 && sell_h != 2 && sell_h != 4)
+        fail(YS_ERR_VALIDATION, "YS_PCG_SELL must be 0, 1, 2 or 4");
+      if (sell_h > 0) sell_build(c, sell_h, false);
+      SellDev sl = sell_dev(c);
       int64_t nb = c.NB;
       const double* minv = c.minv.p;
-      double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *part = c.partials.p,
-             *hist = c.hist.p;
+      double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *hist = c.hist.p;
       PcgState* stp = c.pcg.p;
+      c.gridbar.resize(sizeof(GridBar));
+      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
-      void* args[] = {&d0, &d1, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
-      YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
+      bool launched = false;
+      if (sell_h > 0) {
+        // per-warp plan cache in shared memory; the most CTAs per SM (3, 2, 1) that fit
+        void* kern = sell_h == 1 ? (void*)k_pcg33_sell<1> : sell_h == 2 ? (void*)k_pcg33_sell<2> : (void*)k_pcg33_sell<4>;
+        const int wpb = kTB / 32;
+        for (int per = kSpmvMinB; per >= 1 && !launched; --per) {
+          int gsz = per * sm_count();
+          int K = int(ceil_div(c.sell_slices, int64_t(gsz) * wpb));
+          int TW = sell_max_warp_rows(c, int64_t(gsz) * wpb, K);
+          const size_t smem = size_t(wpb) * K * 8 + size_t(wpb) * K * 32 * 4 + size_t(wpb) * TW * 32 * 4;
+          if (smem > size_t(220 * 1024) / per) continue;
+          YS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          int occ = 0;
+          YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, smem));
+          if (occ < per) continue;
+          c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
+          double* part = c.partials.p;
+          void* args[] = {&sl, &nb, &K, &TW, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
+          YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, smem, s));
+          launched = true;
+        }
+      }
+      if (!launched) {
+        void* kern = sell_h == 0   ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 0>)
+                     : sell_h == 1 ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 1>)
+                     : sell_h == 2 ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 2>)
+                                   : reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 4>);
+        // 256 x 3 CTAs per SM (384 x 2, the same 768 threads, measured equal at C5)
+        int occ = 0;
+        YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+        if (occ < 1) occ = 1;
+        int gsz = occ * sm_count();
+        c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
+        SpmvDev d0 = spmv_dev(c.S[0]);
+        SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+        int h1 = has1 ? 1 : 0;
+        double* part = c.partials.p;
+        void* args[] = {&d0, &d1, &sl, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
+        YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
+      }
       PcgState fin{};
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
