@@ -751,13 +751,11 @@ int ys_apply_hessian(ys_context* c, const double* x, double* y) {
     YS_CUDA(cudaMemcpyAsync(c->r.p, x, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     YS_CUDA(cudaMemcpyAsync(c->hp.p, y, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     static const int variant = getenv("YS_APPLY_VARIANT") ? atoi(getenv("YS_APPLY_VARIANT")) : 0;
-    if (variant >= 40 && variant < 60 && c->uniform3) {
-      // diagnostic: y += H x through a sliced-ELL SpMV variant (ys_time_kernel numbering)
-      const bool sym = variant >= 50;
-      const int h = 1 << ((variant - 40) % 4);
-      sell_build(*c, h, sym);
+    if (variant >= 40 && variant < 44 && c->uniform3) {
+      // diagnostic: y += H x through the sliced-ELL copy with 2^(variant-40) lanes per row
+      sell_build(*c, 1 << (variant - 40));
       c->z.resize(c->s + 2);
-      spmv_sell(*c, c->r.p, c->z.p, true);
+      spmv_sell(*c, c->r.p, c->z.p);
       std::vector<double> t(c->s);
       YS_CUDA(cudaMemcpyAsync(t.data(), c->z.p, c->s * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       YS_CUDA(cudaStreamSynchronize(c->stream));
@@ -1158,12 +1156,10 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
     cudaStream_t s = c->stream;
     double alg = 0.0;
     auto launch = [&]() {
-      if (which >= 40 && which < 60) {
-        // sliced-ELL SpMV: full copy 40-43 (H = 1, 2, 4, 8), its build 44-47, default-policy loads 48/49 (H = 4/8);
-        // symmetric upper copy + transposed slots 50-53 (H = 1, 2, 4, 8), its build 54-57
-        if (which >= 44 && which < 48) sell_build(*c, 1 << (which - 44), false);
-        else if (which >= 54 && which < 58) sell_build(*c, 1 << (which - 54), true);
-        else spmv_sell(*c, c->p.p, c->hp.p, which < 48 || (which >= 50 && which < 58));
+      if (which >= 40 && which < 48) {
+        // sliced-ELL copy of the PCG: SpMV 40-43 (H = 1, 2, 4, 8 lanes per row), its build 44-47
+        if (which >= 44) sell_build(*c, 1 << (which - 44));
+        else spmv_sell(*c, c->p.p, c->hp.p);
       } else if (which == 5 || which == 6) {  // 1000 counter grid barriers per launch (6: + partial reductions)
         barrier_probe(*c, 1000, which == 6 ? 3 : 2);
       } else if (which >= 10) {
@@ -1177,17 +1173,7 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
         ctx_eval_all(*c, true, true);
       }
     };
-    if (which >= 40 && which < 44) sell_build(*c, 1 << (which - 40), false);
-    if (which == 48 || which == 49) sell_build(*c, which == 48 ? 4 : 8, false);
-    if (which >= 50 && which < 54) sell_build(*c, 1 << (which - 50), true);
-    if (which == 58 || which == 59) sell_build(*c, which == 58 ? 2 : 4, true);  // + 2 CTAs per SM
-    {
-      // YS_L2_PERSIST=<fraction of the max set-aside>: L2 window over the streamed matrix copy
-      const char* e = getenv("YS_L2_PERSIST");
-      const double f = e ? atof(e) : 0.0;
-      if ((which >= 40 && which < 44) || which == 48 || which == 49) l2_persist(*c, c->sell_val.p, c->sell_rows * 288 * sizeof(double), f);
-      else if (which == 0) l2_persist(*c, c->S[0].values.p, c->S[0].n_values * sizeof(double), f);
-    }
+    if (which >= 40 && which < 44) sell_build(*c, 1 << (which - 40));
     if (which == 0 || which >= 10) {
       c->p.resize(c->s + 2);
       c->hp.resize(c->s + 2);
@@ -1212,8 +1198,6 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
     float ms = 0.f;
     YS_CUDA(cudaEventElapsedTime(&ms, c->ev[7], c->ev[8]));
     *avg_ms = double(ms) / reps;
-    l2_persist(*c, nullptr, 0, 0.0);
-    cudaCtxResetPersistingL2Cache();
     if (bytes) *bytes = alg;
   });
 }

@@ -214,9 +214,6 @@ struct Context {
   DevBuf<int32_t> sell_len, sell_col;
   DevBuf<int64_t> sell_soff;
   DevBuf<double> sell_val;
-  DevBuf<int32_t> sell_tpos, sell_tstart, sell_utpos0, sell_utpos1;  // symmetric (upper-only) mode
-  DevBuf<double> sell_slots;
-  bool sell_sym = false;
   DevBuf<int> sell_tw;  // max entry rows per warp (persistent PCG plan cache)
   int sell_h = 0;
   int64_t sell_rows = 0, sell_slices = 0;  // entry rows, slices
@@ -289,9 +286,8 @@ void spmv_structure(Context& c, Structure& st, const BlocksDev& blocks, const do
 
 BlocksDev blocks_view(Context& c);
 void drop_pcg_graph(Context& c);
-void sell_build(Context& c, int lanes_per_row, bool sym);  // ys_sell.cu
-void spmv_sell(Context& c, const double* x, double* y, bool streaming = true);
-size_t l2_persist(Context& c, const void* base, size_t bytes, double frac);
+void sell_build(Context& c, int lanes_per_row);  // ys_sell.cu
+void spmv_sell(Context& c, const double* x, double* y);
 int sell_max_warp_rows(Context& c, int64_t warps, int slices_per_warp);   // y = H x through the sliced-ELL copy
 bool pcg_uses_conditional_graph(Context& c);
 

@@ -1,14 +1,21 @@
 // ys_sell.cu — builds the PCG's sliced-ELL full copy of H (ys_sell.cuh) from
 // the static and dynamic upper-storage structures, once per solve.
 //
-// Cost at C5 (3.0 M full entries): one pass reading the 117 MB of upper
-// blocks twice (own + transposed) and writing ~230 MB — a few tens of
+// Cost at C5 (3.0 M full entries): one pass reading the upper blocks twice
+// (own + transposed) and writing the ~230 MB copy — a few hundred
 // microseconds against the ~420 SpMVs of the solve that then stream it.
+//
+// Measured and rejected (C5, B200, profiles/r01_pcg_sell_c5.md):
+//  * a symmetric copy — upper blocks streamed once, B^T x_R stored to a
+//    per-column-row slot (32 B, sector aligned), slot runs summed after the
+//    barrier: 137 MB instead of ~260 MB per SpMV, but the scattered slot
+//    stores and the slot gathers made phases A + B 140 us vs 56 us;
+//  * an L2 persisting window over the copy (83 MB set-aside): 49 -> 51-56 us;
+//  * bulk L2 prefetch (cp.async.bulk.prefetch) of each warp's next slice:
+//    49 -> 58 us.
 #include <cub/cub.cuh>
 
 #include <algorithm>
-#include <cstdio>
-#include <cstdlib>
 
 #include "ys_sell.cuh"
 
@@ -20,25 +27,10 @@ __device__ __forceinline__ int row_entries(const SpmvDev& S, int64_t R) {
   return (S.nrow[R + 1] - S.nrow[R]) + (S.trow[R + 1] - S.trow[R]);
 }
 
-__global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, int sym, int32_t* len, int32_t* tcnt) {
+__global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, int32_t* len) {
   const int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (R >= nb) return;
-  if (!sym) {
-    len[R] = row_entries(S0, R) + (has1 ? row_entries(S1, R) : 0);
-    return;
-  }
-  len[R] = (S0.nrow[R + 1] - S0.nrow[R]) + (has1 ? S1.nrow[R + 1] - S1.nrow[R] : 0);
-  tcnt[R] = (S0.trow[R + 1] - S0.trow[R]) + (has1 ? S1.trow[R + 1] - S1.trow[R] : 0);
-}
-
-// Symmetric mode: slot of every off-diagonal upper block u = first slot of its
-// column row + static transposed entries before it (dynamic after static).
-__global__ void k_sell_utpos(SpmvDev S, int64_t nb, const int32_t* tstart, SpmvDev S0, int is_dyn, int32_t* utpos) {
-  const int64_t C = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (C >= nb) return;
-  const int32_t base = tstart[C] + (is_dyn ? S0.trow[C + 1] - S0.trow[C] : 0);
-  const int32_t j0 = S.trow[C], j1 = S.trow[C + 1];
-  for (int32_t j = j0; j < j1; ++j) utpos[S.tlist[j].x] = base + (j - j0);
+  len[R] = row_entries(S0, R) + (has1 ? row_entries(S1, R) : 0);
 }
 
 // width of slice s (in entry rows) = max over its rows of ceil(len / H)
@@ -60,17 +52,15 @@ struct SellOut {
   int32_t* col;
   double* val;
   int H;
-  int32_t* tpos;  // symmetric mode
 };
 
 __device__ __forceinline__ void put_entry(const SellOut& o, int64_t R, int k, int32_t xcol, const double* __restrict__ b,
-                                          bool transpose, int32_t tp = -1) {
+                                          bool transpose) {
   const int rps = 32 / o.H;
   const int64_t slice = R / rps;
   const int lane = int(R % rps) * o.H + k % o.H;
   const int64_t e = o.soff[slice] + k / o.H;
   o.col[e * 32 + lane] = xcol;
-  if (o.tpos) o.tpos[e * 32 + lane] = tp;
   double v[9];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -91,69 +81,18 @@ __device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int
   return k;
 }
 
-__device__ __forceinline__ int fill_upper(const SpmvDev& S, const SellOut& o, int64_t R, int k, const int32_t* utpos) {
-  for (int32_t u = S.nrow[R]; u < S.nrow[R + 1]; ++u) {
-    const int32_t c = S.col[u];
-    put_entry(o, R, k++, c, S.values + 9 * int64_t(u), false, c == 3 * int32_t(R) ? -1 : utpos[u]);
-  }
-  return k;
-}
-
 // One thread per block row; the threads of a slice write the same entry row
 // together (coalesced stores).
-__global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, SellOut o, const int32_t* utpos0,
-                            const int32_t* utpos1) {
+__global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, SellOut o) {
   const int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (R >= nb) return;
-  if (o.tpos) {
-    const int k = fill_upper(S0, o, R, 0, utpos0);
-    if (has1) fill_upper(S1, o, R, k, utpos1);
-    return;
-  }
   int k = fill_from(S0, o, R, 0);
   if (has1) fill_from(S1, o, R, k);
 }
 
-// Symmetric mode, standalone: pass 1 (own products + transposed slots) and
-// pass 2 (add the slot runs).
-template <int H, int MINB>
-__global__ void __launch_bounds__(kTB, MINB) k_spmv_usell1(SellDev S, const double* __restrict__ x,
-                                                                double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t sl = w0; sl < S.nslices; sl += nw) {
-    double a[3] = {0.0, 0.0, 0.0}, dg[3] = {0.0, 0.0, 0.0};
-    int64_t R;
-    usell_acc<H>(S, sl, lane, x, a, dg, R);
-    if (lane % H == 0 && R < S.nb) {
-      y[3 * R] = a[0];
-      y[3 * R + 1] = a[1];
-      y[3 * R + 2] = a[2];
-    }
-  }
-}
-
-__global__ void k_spmv_usell2(SellDev S, double* __restrict__ y) {
-  constexpr int SW = 4;
-  const int lane = threadIdx.x % SW;
-  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
-  const int64_t g0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
-  const int64_t ng = int64_t(gridDim.x) * blockDim.x / SW;
-  for (int64_t R = g0; R < S.nb; R += ng) {
-    double t[3];
-    usell_tsum<SW>(S, R, lane, mask, t);
-    if (lane == 0) {
-      y[3 * R] += t[0];
-      y[3 * R + 1] += t[1];
-      y[3 * R + 2] += t[2];
-    }
-  }
-}
-
-// Standalone y = H x through the sliced-ELL copy (timing diagnostics and the
-// non-persistent path): one slice per warp, grid-stride.
-template <int H, bool ST>
+// Standalone y = H x through the sliced-ELL copy (ys_time_kernel and
+// YS_APPLY_VARIANT diagnostics): one slice per warp, grid-stride.
+template <int H>
 __global__ void __launch_bounds__(kTB, kSpmvMinB) k_spmv_sell(SellDev S, const double* __restrict__ x,
                                                               double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
@@ -162,7 +101,7 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_spmv_sell(SellDev S, const d
   for (int64_t sl = w0; sl < S.nslices; sl += nw) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     int64_t R;
-    sell_acc<H, ST>(S, sl, lane, x, a0, a1, a2, R);
+    sell_acc<H>(S, sl, lane, x, a0, a1, a2, R);
     if (lane % H == 0 && R < S.nb) {
       y[3 * R] = a0;
       y[3 * R + 1] = a1;
@@ -200,18 +139,13 @@ int sell_max_warp_rows(Context& c, int64_t NW, int K) {
 }
 
 SellDev sell_dev(Context& c) {
-  return SellDev{c.sell_len.p,  c.sell_soff.p,
-                 c.sell_col.p,  c.sell_val.p,
-                 c.NB,          c.sell_slices,
-                 c.sell_sym ? c.sell_tpos.p : nullptr,
-                 c.sell_sym ? c.sell_tstart.p : nullptr,
-                 c.sell_sym ? c.sell_slots.p : nullptr};
+  return SellDev{c.sell_len.p, c.sell_soff.p, c.sell_col.p, c.sell_val.p, c.NB, c.sell_slices};
 }
 
 // Builds the sliced-ELL copy of S[0] + S[1] (uniform 3x3 systems only) with H
 // lanes per block row.  One host synchronisation (the entry-row count sizes
 // the buffers).
-void sell_build(Context& c, int H, bool sym) {
+void sell_build(Context& c, int H) {
   cudaStream_t s = c.stream;
   const bool has1 = c.S[1].n_blocks > 0;
   SpmvDev d0 = spmv_dev(c.S[0]);
@@ -220,7 +154,6 @@ void sell_build(Context& c, int H, bool sym) {
   const int rps = 32 / H;
   const int64_t nsl = ceil_div(nb, rps);
   c.sell_h = H;
-  c.sell_sym = sym;
   c.sell_slices = nsl;
   c.sell_len.resize(size_t(std::max<int64_t>(nb, 1)));
   c.sell_soff.resize(size_t(nsl + 1));
@@ -228,9 +161,7 @@ void sell_build(Context& c, int H, bool sym) {
     c.sell_rows = 0;
     return;
   }
-  if (sym) c.sell_tstart.resize(size_t(nb + 1));
-  k_sell_len<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, nb, sym ? 1 : 0, c.sell_len.p,
-                                                    sym ? c.sell_tstart.p + 1 : nullptr);
+  k_sell_len<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, nb, c.sell_len.p);
   k_sell_width<<<int(ceil_div(nsl, kTB)), kTB, 0, s>>>(c.sell_len.p, nb, H, nsl, c.sell_soff.p);
   YS_LAUNCH_CHECK();
   int64_t* so = c.sell_soff.p;
@@ -239,109 +170,29 @@ void sell_build(Context& c, int H, bool sym) {
   YS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, so, so, n, s));
   c.cubtmp.resize(std::max<size_t>(bytes, 1));
   YS_CUDA(cub::DeviceScan::InclusiveSum(c.cubtmp.p, bytes, so, so, n, s));
-  int64_t rows[2] = {0, 0};
-  YS_CUDA(cudaMemcpyAsync(&rows[0], so + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  if (sym) {
-    int32_t* ts = c.sell_tstart.p;
-    YS_CUDA(cudaMemsetAsync(ts, 0, sizeof(int32_t), s));
-    const int nt = int(nb + 1);
-    YS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, ts, ts, nt, s));
-    c.cubtmp.resize(std::max<size_t>(bytes, 1));
-    YS_CUDA(cub::DeviceScan::InclusiveSum(c.cubtmp.p, bytes, ts, ts, nt, s));
-    c.sell_utpos0.resize(size_t(std::max<int64_t>(c.S[0].n_blocks, 1)));
-    c.sell_utpos1.resize(size_t(std::max<int64_t>(c.S[1].n_blocks, 1)));
-    k_sell_utpos<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, nb, ts, d0, 0, c.sell_utpos0.p);
-    if (has1) k_sell_utpos<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d1, nb, ts, d0, 1, c.sell_utpos1.p);
-    YS_LAUNCH_CHECK();
-    int32_t nslot = 0;
-    YS_CUDA(cudaMemcpyAsync(&nslot, ts + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    YS_CUDA(cudaStreamSynchronize(s));
-    rows[1] = nslot;
-    c.sell_slots.resize(size_t(4 * rows[1] + 4));
-  }
+  int64_t rows = 0;
+  YS_CUDA(cudaMemcpyAsync(&rows, so + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   YS_CUDA(cudaStreamSynchronize(s));
-  c.sell_rows = rows[0];
-  c.sell_col.resize(size_t(rows[0] * 32 + 4));
-  c.sell_val.resize(size_t(rows[0] * 288 + 4));
-  if (sym) c.sell_tpos.resize(size_t(rows[0] * 32 + 4));
-  k_sell_fill<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(
-      d0, d1, has1 ? 1 : 0, nb, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, sym ? c.sell_tpos.p : nullptr},
-      c.sell_utpos0.p, c.sell_utpos1.p);
+  c.sell_rows = rows;
+  c.sell_col.resize(size_t(rows * 32 + 4));
+  c.sell_val.resize(size_t(rows * 288 + 4));
+  k_sell_fill<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, nb,
+                                                     SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H});
   YS_LAUNCH_CHECK();
 }
 
-// L2 residency of a streamed buffer: persisting-lines window over [base,
-// base + bytes) on the context stream; frac scales the device's maximum
-// persisting set-aside (0 clears the window).  Returns the bytes marked.
-size_t l2_persist(Context& c, const void* base, size_t bytes, double frac) {
-  static int max_persist = -1, max_window = 0;
-  if (max_persist < 0) {
-    YS_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c.device));
-    YS_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c.device));
-  }
-  cudaStreamAttrValue a = {};
-  if (frac <= 0.0 || bytes == 0 || max_persist <= 0) {
-    a.accessPolicyWindow.num_bytes = 0;
-    YS_CUDA(cudaStreamSetAttribute(c.stream, cudaStreamAttributeAccessPolicyWindow, &a));
-    return 0;
-  }
-  const size_t set_aside = size_t(double(max_persist) * std::min(frac, 1.0));
-  YS_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside));
-  const size_t win = std::min(bytes, size_t(max_window));
-  a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  a.accessPolicyWindow.num_bytes = win;
-  a.accessPolicyWindow.hitRatio = float(std::min(1.0, double(set_aside) / double(win)));
-  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  YS_CUDA(cudaStreamSetAttribute(c.stream, cudaStreamAttributeAccessPolicyWindow, &a));
-  fprintf(stderr, "[ys] L2 persist: max set-aside %d B, max window %d B, window %zu B, hitRatio %.3f\n", max_persist,
-          max_window, win, double(a.accessPolicyWindow.hitRatio));
-  return size_t(double(win) * a.accessPolicyWindow.hitRatio);
-}
-
-template <int H, bool ST = true>
+template <int H>
 static void launch_sell(Context& c, const double* x, double* y) {
   int occ = 0;
-  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell<H, ST>, kTB, 0));
+  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_sell<H>, kTB, 0));
   const int64_t warps = c.sell_slices;
   const int g = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(std::max(occ, 1)) * sm_count(),
                                                            ceil_div(warps * 32, kTB))));
-  k_spmv_sell<H, ST><<<g, kTB, 0, c.stream>>>(sell_dev(c), x, y);
+  k_spmv_sell<H><<<g, kTB, 0, c.stream>>>(sell_dev(c), x, y);
   YS_LAUNCH_CHECK();
 }
 
-template <int H, int MINB = kSpmvMinB>
-static void launch_usell(Context& c, const double* x, double* y) {
-  int occ = 0;
-  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv_usell1<H, MINB>, kTB, 0));
-  const int g = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(std::max(occ, 1)) * sm_count(),
-                                                           ceil_div(c.sell_slices * 32, kTB))));
-  static const int pass = getenv("YS_USELL_PASS") ? atoi(getenv("YS_USELL_PASS")) : 3;  // diagnostic: 1, 2 or both
-  if (pass & 1) k_spmv_usell1<H, MINB><<<g, kTB, 0, c.stream>>>(sell_dev(c), x, y);
-  if (pass & 2)
-    k_spmv_usell2<<<int(std::min<int64_t>(ceil_div(c.NB * 4, kTB), 8 * sm_count())), kTB, 0, c.stream>>>(sell_dev(c),
-                                                                                                     y);
-  YS_LAUNCH_CHECK();
-}
-
-void spmv_sell(Context& c, const double* x, double* y, bool streaming) {
-  if (c.sell_sym && !streaming) {  // diagnostic: 2 CTAs per SM (no spills)
-    if (c.sell_h == 2) return launch_usell<2, 2>(c, x, y);
-    if (c.sell_h == 4) return launch_usell<4, 2>(c, x, y);
-  }
-  if (c.sell_sym) {
-    switch (c.sell_h) {
-      case 1: return launch_usell<1>(c, x, y);
-      case 2: return launch_usell<2>(c, x, y);
-      case 4: return launch_usell<4>(c, x, y);
-      case 8: return launch_usell<8>(c, x, y);
-      default: fail(YS_ERR_INTERNAL, "sliced-ELL SpMV: unsupported lanes per row");
-    }
-  }
-  if (!streaming) {  // diagnostic: default-policy loads
-    if (c.sell_h == 4) return launch_sell<4, false>(c, x, y);
-    if (c.sell_h == 8) return launch_sell<8, false>(c, x, y);
-  }
+void spmv_sell(Context& c, const double* x, double* y) {
   switch (c.sell_h) {
     case 1: launch_sell<1>(c, x, y); break;
     case 2: launch_sell<2>(c, x, y); break;

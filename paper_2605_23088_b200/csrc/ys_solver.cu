@@ -1085,7 +1085,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       }();
       if (sell_h != 0 && sell_h != 1 && sell_h != 2 && sell_h != 4)
         fail(YS_ERR_VALIDATION, "YS_PCG_SELL must be 0, 1, 2 or 4");
-      if (sell_h > 0) sell_build(c, sell_h, false);
+      if (sell_h > 0) sell_build(c, sell_h);
       SellDev sl = sell_dev(c);
       int64_t nb = c.NB;
       const double* minv = c.minv.p;

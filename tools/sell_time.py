@@ -19,12 +19,11 @@ for k in range(3):
     eng.bump_dynamic_epoch()
     st = eng.minimize_step(cfg.pcg_tol, -1, want_dx=False)
 ms, launches, nevd = eng.stage_times(True)
-print(f"{name} L2={os.environ.get('YS_L2_PERSIST')} YS_PCG_SELL={os.environ.get('YS_PCG_SELL')} pcg_it={st.pcg_iterations} res={st.pcg_residual:.6e} "
+print(f"{name} YS_PCG_SELL={os.environ.get('YS_PCG_SELL')} pcg_it={st.pcg_iterations} res={st.pcg_residual:.6e} "
       f"total={ms[6]:.3f} pcg={ms[4]:.3f} per-it={1e3*ms[4]/max(st.pcg_iterations,1):.1f}us "
       f"phases={[round(1e3*v/max(st.pcg_iterations,1), 2) for v in ms[8:12]]}", flush=True)
-VARIANTS = [(0, "row gather k_spmv33"), (42, "sell H=4"), (43, "sell H=8"), (46, "sell build H=4"),
-                     (50, "usell H=1"), (51, "usell H=2"), (52, "usell H=4"), (53, "usell H=8"),
-                     (58, "usell H=2 minb2"), (59, "usell H=4 minb2"), (56, "usell build H=4")]
+VARIANTS = [(0, "row gather k_spmv33"), (40, "sell H=1"), (41, "sell H=2"), (42, "sell H=4"), (43, "sell H=8"),
+            (46, "sell build H=4")]
 only = os.environ.get("SELL_VARIANTS")
 if only:
     keep = {int(v) for v in only.split(",")}
