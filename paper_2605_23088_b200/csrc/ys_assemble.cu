@@ -19,6 +19,7 @@
 //      one) and inverts it for the preconditioner.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "ys_device.cuh"
 
@@ -168,23 +169,45 @@ __global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const doubl
 
 // Pass B: Jacobi EVD + clamp + reconstruction for the compacted indefinite
 // elements only (fully populated warps), then the vertex blocks.
+//
+// Pass B batched over up to kStencilBatch energies of one kind (C5: the 8 soft
+// bodies): one launch whose grid-stride loop spans every energy's compacted
+// list, so the ~9 EVDs per thread leave no per-energy tail (8 launches of
+// ~1.2 EVDs per resident thread lost about half the SMs to the tail).
+constexpr int kStencilBatch = 8;
+struct StencilBatch {
+  int n;
+  EnergyDev e[kStencilBatch];
+  double* hc[kStencilBatch];
+  const unsigned int* count[kStencilBatch];
+  int64_t base[kStencilBatch];  // first list / M slot of each energy
+};
+
 template <int KIND>
-__global__ void __launch_bounds__(128) k_eval_stencil_b(EnergyDev E, double* __restrict__ hc,
-                                                        const unsigned int* __restrict__ count,
-                                                        const int32_t* __restrict__ list,
-                                                        const double* __restrict__ mbuf) {
-  const unsigned n = *count;
-  const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
-  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int64_t i = list[k];
+__global__ void __launch_bounds__(128) k_eval_stencil_b_batch(const __grid_constant__ StencilBatch B,
+                                                              const int32_t* __restrict__ list,
+                                                              const double* __restrict__ mbuf) {
+  unsigned pre[kStencilBatch + 1];
+  pre[0] = 0;
+#pragma unroll
+  for (int j = 0; j < kStencilBatch; ++j) pre[j + 1] = pre[j] + (j < B.n ? *B.count[j] : 0u);
+  const unsigned total = pre[kStencilBatch];
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    int j = 0;
+#pragma unroll
+    for (int q = 1; q < kStencilBatch; ++q) j += k >= pre[q] ? 1 : 0;
+    const EnergyDev& E = B.e[j];
+    const int64_t slot = B.base[j] + (k - pre[j]);
+    const int64_t i = list[slot];
     double m[45];
-    const double* src = mbuf + 45 * int64_t(k);
+    const double* src = mbuf + 45 * slot;
 #pragma unroll
     for (int q = 0; q < 45; ++q) m[q] = src[q];
     psd_project9(m);
     const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
     const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
-    const VertexBlockWriter wr{hc + inst_hoff(E, i), vertex_pair_swaps(gs)};
+    const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
+    const VertexBlockWriter wr{B.hc[j] + inst_hoff(E, i), vertex_pair_swaps(gs)};
     expand_vertex_blocks(m, full, wr);
   }
 }
@@ -649,6 +672,50 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
   cudaStream_t s = c.stream;
   c.evd_count.resize(std::max(c.evd_count.n, c.energies.size()));
   c.evd_count.zero(s);
+  // every stencil energy gets its own compacted-list / M range, so pass B can
+  // run once for all energies of a kind after their pass A
+  int64_t evd_total = 0;
+  std::vector<int64_t> evd_base(c.energies.size(), 0);
+  for (size_t id = 0; id < c.energies.size(); ++id) {
+    const Energy& e = c.energies[id];
+    if ((e.kind == K_SNH || e.kind == K_BENDING) && e.n > 0) {
+      evd_base[id] = evd_total;
+      evd_total += e.n;
+    }
+  }
+  c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * evd_total)));
+  c.evd_list.resize(std::max(c.evd_list.n, size_t(evd_total)));
+  const bool pass_b = with_hessian && project;
+  // pass B (Jacobi EVD of the indefinite elements) can run batched over
+  // pending stencil energies of one kind (YS_EVD_BATCH = elements per batch).
+  // Default: right after each energy's pass A, while its M buffer (360 B per
+  // indefinite element) sits in L2.  C5 (8 bodies of 127k tets), eval stage:
+  // per energy 4.93 ms, batches of 2 bodies 5.0, 4 bodies 5.4, all 8 6.4 ms.
+  static const int64_t kBatchElems = getenv("YS_EVD_BATCH") ? atoll(getenv("YS_EVD_BATCH")) : 1;
+  const unsigned gb = unsigned(sm_count() * 4);
+  std::vector<size_t> pending;
+  int pending_kind = -1;
+  int64_t pending_n = 0;
+  auto flush = [&]() {
+    if (pending.empty()) return;
+    StencilBatch B{};
+    B.n = int(pending.size());
+    for (int j = 0; j < B.n; ++j) {
+      Energy& e = c.energies[pending[j]];
+      B.e[j] = energy_dev(c, e);
+      B.hc[j] = c.S[e.dynamic ? 1 : 0].hcontrib.p;
+      B.count[j] = c.evd_count.p + pending[j];
+      B.base[j] = evd_base[pending[j]];
+    }
+    if (pending_kind == 0)
+      k_eval_stencil_b_batch<0><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+    else
+      k_eval_stencil_b_batch<1><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+    YS_LAUNCH_CHECK();
+    ++c.launches;
+    pending.clear();
+    pending_n = 0;
+  };
   for (size_t id = 0; id < c.energies.size(); ++id) {
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
@@ -658,20 +725,25 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
     switch (e.kind) {
       case K_SNH:
       case K_BENDING: {
-        c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * e.n)));
-        c.evd_list.resize(std::max(c.evd_list.n, size_t(e.n)));
         unsigned int* cnt = c.evd_count.p + id;
-        const unsigned ga = grid_for(e.n, 128), gb = unsigned(sm_count() * 4);
-        if (e.kind == K_SNH) {
+        const unsigned ga = grid_for(e.n, 128);
+        int32_t* lst = c.evd_list.p + evd_base[id];
+        double* mb = c.evd_m.p + 45 * evd_base[id];
+        const int kind = e.kind == K_SNH ? 0 : 1;
+        if (kind == 0)
           k_eval_stencil_a<0><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
-                                                 c.evd_list.p, c.evd_m.p);
-          if (wh && proj) k_eval_stencil_b<0><<<gb, 128, 0, s>>>(E, st.hcontrib.p, cnt, c.evd_list.p, c.evd_m.p);
-        } else {
+                                                 lst, mb);
+        else
           k_eval_stencil_a<1><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
-                                                 c.evd_list.p, c.evd_m.p);
-          if (wh && proj) k_eval_stencil_b<1><<<gb, 128, 0, s>>>(E, st.hcontrib.p, cnt, c.evd_list.p, c.evd_m.p);
+                                                 lst, mb);
+        YS_LAUNCH_CHECK();
+        if (pass_b) {
+          if (pending_kind != kind || int(pending.size()) == kStencilBatch) flush();
+          pending_kind = kind;
+          pending.push_back(id);
+          pending_n += e.n;
+          if (pending_n >= kBatchElems) flush();
         }
-        ++c.launches;
         break;
       }
       case K_ORTHO:
@@ -695,6 +767,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
     YS_LAUNCH_CHECK();
     ++c.launches;
   }
+  flush();
 }
 
 void ctx_gather_all(Context& c) {
