@@ -88,14 +88,18 @@ for name, lst in per.items():
 open(os.path.join(out, f"{tag}_ncu_top_{scene}.md"), "w").write("\n".join(tl) + "\n")
 js = os.path.join(out, "ncu_summary.json")
 d = json.load(open(js)) if os.path.exists(js) else {}
-sp = [v for k, v in summary.items() if k.startswith("k_spmv_sell")] or \
-     [v for k, v in summary.items() if k.startswith("k_spmv33")]
+def base(k):
+    return k.split("::")[-1]
+
+
+sp = [v for k, v in summary.items() if base(k).startswith("k_spmv_sell")] or \
+     [v for k, v in summary.items() if base(k).startswith("k_spmv33")]
 prev = d.get(scene, {})
-d[scene] = dict(prev, tag=tag, kernels=dict(prev.get("kernels", {}), **summary))
+d[scene] = dict(prev, tag=tag, kernels=summary)
 if sp:
     d[scene]["spmv_dram_bytes"] = 1e6 * (sp[0]["dram__bytes_read.sum"] + sp[0]["dram__bytes_write.sum"])
-pp = [v for k, v in summary.items() if k.startswith("k_pcg33_sell")] or \
-     [v for k, v in summary.items() if k.startswith("k_pcg33_persistent")]
+pp = [v for k, v in summary.items() if base(k).startswith("k_pcg33_sell")] or \
+     [v for k, v in summary.items() if base(k).startswith("k_pcg33_persistent")]
 if pp and pcg_iters:
     d[scene]["pcg_iterations"] = pcg_iters
     d[scene]["pcg_dram_bytes_per_iteration"] = 1e6 * (pp[0]["dram__bytes_read.sum"] +
