@@ -694,38 +694,45 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
 }
 
 // ---------------------------------------------------------------------------
-// Persistent PCG over the sliced-ELL copy (ys_sell.cuh).
-//
-// Warp w of CTA b owns the slices gw + k * NW (gw = b * 8 + w, k < K) for the
-// whole solve.  Its SpMV plan — each slice's first entry row, each lane's
-// entry count and the column DoFs of all its entries — is loaded into shared
-// memory once, so every SpMV issues the x gathers together with the value
-// stream (no soff -> col -> x dependency chain per slice): C5 phase A 51 ->
-// 45 us.  Phases B and C keep one thread per block row over global vectors
+// Persistent PCG over a streamed copy of H (ys_sell.cuh): one cooperative
+// launch per solve.  Phase A (SpMV + pHp partials) is a policy:
+//  * SellPhaseA — the sliced-ELL full copy: warp w of CTA b owns the slices
+//    gw + k NW (gw = b * 8 + w, k < K).  Its SpMV plan (each slice's first
+//    entry row, each lane's entry count, the column DoFs of all its entries)
+//    is loaded into shared memory once, so every SpMV issues the x gathers
+//    together with the value stream (C5 phase A 51 -> 45 us);
+//  (a warp-range symmetric copy — Morton-ordered row ranges per warp, blocks
+//   inside a range stored once with their transposed products through
+//   shared-memory slots — cut the entries by ~20% but not the time: phase A
+//   45.1 vs 44.7 us at C5, 26.2 vs 17.6 us at C4; profiles/r01_pcg_sell_c5.md)
+// Phases B and C keep one thread per block row over global vectors
 // (independent loads; a shared-memory row state with the slice mapping was
 // measured slower: its per-row chains are latency-bound).  Fixed-order
 // reductions (deterministic).
-template <int H>
-__global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_sell(SellDev SL, int64_t nb, int K, int TW,
-                                                             const double* __restrict__ minv, double* __restrict__ x,
-                                                             double* __restrict__ r, double* __restrict__ z,
-                                                             double* __restrict__ p, double* __restrict__ hp,
-                                                             PcgState* st, double* part, double* hist, GridBar* gb) {
-  extern __shared__ double smem[];
-  constexpr int RPS = 32 / H;
-  constexpr int WPB = kTB / 32;
-  const int G = gridDim.x;
-  const int warp = threadIdx.x >> 5, wl = threadIdx.x & 31;
-  const int grp = wl / H, h = wl % H;
-  const int64_t gw = int64_t(blockIdx.x) * WPB + warp;
-  const int64_t NW = int64_t(G) * WPB;
-  // plan: per warp K int2 {first entry row, local entry-row offset}, K x 32
-  // lane counts, TW x 32 column DoFs
-  int2* meta = reinterpret_cast<int2*>(smem) + warp * K;
-  int32_t* lhs = reinterpret_cast<int32_t*>(reinterpret_cast<int2*>(smem) + WPB * K) + warp * K * 32;
-  int32_t* cols = lhs + (WPB - warp) * K * 32 + warp * TW * 32;
-  const int kn = gw < SL.nslices ? int(min(int64_t(K), (SL.nslices - gw + NW - 1) / NW)) : 0;
-  {
+struct SellPhaseA {
+  SellDev SL;
+  int64_t nb;
+  int K, TW;
+  int2* meta;
+  int32_t* lhs;
+  int32_t* cols;
+  int kn, wl, grp, h, warp;
+  int64_t gw, NW;
+
+  __device__ void prologue(double* smem) {
+    constexpr int H = 4, RPS = 32 / H, WPB = kTB / 32;
+    warp = threadIdx.x >> 5;
+    wl = threadIdx.x & 31;
+    grp = wl / H;
+    h = wl % H;
+    gw = int64_t(blockIdx.x) * WPB + warp;
+    NW = int64_t(gridDim.x) * WPB;
+    // per warp K int2 {first entry row, local entry-row offset}, K x 32 lane
+    // counts, TW x 32 column DoFs
+    meta = reinterpret_cast<int2*>(smem) + warp * K;
+    lhs = reinterpret_cast<int32_t*>(reinterpret_cast<int2*>(smem) + WPB * K) + warp * K * 32;
+    cols = lhs + (WPB - warp) * K * 32 + warp * TW * 32;
+    kn = gw < SL.nslices ? int(min(int64_t(K), (SL.nslices - gw + NW - 1) / NW)) : 0;
     int off = 0;
     for (int k = 0; k < kn; ++k) {
       const int64_t sl = gw + k * NW;
@@ -740,6 +747,37 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_sell(SellDev SL, int64
     }
     __syncwarp();
   }
+
+  // hp = H p for the warp's rows; returns this thread's pHp partial
+  __device__ double run(const double* __restrict__ p, double* __restrict__ hp) {
+    constexpr int H = 4, RPS = 32 / H;
+    double dot = 0.0;
+    for (int k = 0; k < kn; ++k) {
+      const int2 m = meta[k];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2);
+      const int64_t R = (gw + k * NW) * RPS + grp;
+      if (h == 0 && R < nb) {
+        double* yo = hp + 3 * R;
+        yo[0] = a0;
+        yo[1] = a1;
+        yo[2] = a2;
+        dot += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
+      }
+    }
+    return dot;
+  }
+};
+
+template <class PA>
+__global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t nb, const double* __restrict__ minv,
+                                                               double* __restrict__ x, double* __restrict__ r,
+                                                               double* __restrict__ z, double* __restrict__ p,
+                                                               double* __restrict__ hp, PcgState* st, double* part,
+                                                               double* hist, GridBar* gb) {
+  extern __shared__ double smem[];
+  const int G = gridDim.x;
+  A.prologue(smem);
   const double gnorm = st->gnorm;
   const double tol = st->tol;
   const long long max_iter = st->max_iter;
@@ -753,20 +791,7 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_sell(SellDev SL, int64
   unsigned long long t0 = gtimer();
   while (status == 0) {
     // ---- phase A: hp = H p, pHp partials
-    double dot[1] = {0.0};
-    for (int k = 0; k < kn; ++k) {
-      const int2 m = meta[k];
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2);
-      const int64_t R = (gw + k * NW) * RPS + grp;
-      if (h == 0 && R < nb) {
-        double* yo = hp + 3 * R;
-        yo[0] = a0;
-        yo[1] = a1;
-        yo[2] = a2;
-        dot[0] += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
-      }
-    }
+    double dot[1] = {A.run(p, hp)};
     block_reduce<1>(dot);
     if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
     grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
@@ -1085,7 +1110,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       }();
       if (sell_h != 0 && sell_h != 1 && sell_h != 2 && sell_h != 4)
         fail(YS_ERR_VALIDATION, "YS_PCG_SELL must be 0, 1, 2 or 4");
-      if (sell_h > 0) sell_build(c, sell_h);
+      if (sell_h > 0 && sell_h != 4) sell_build(c, sell_h);
       SellDev sl = sell_dev(c);
       int64_t nb = c.NB;
       const double* minv = c.minv.p;
@@ -1095,9 +1120,11 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
       bool launched = false;
-      if (sell_h > 0) {
-        // per-warp plan cache in shared memory; the most CTAs per SM (3, 2, 1) that fit
-        void* kern = sell_h == 1 ? (void*)k_pcg33_sell<1> : sell_h == 2 ? (void*)k_pcg33_sell<2> : (void*)k_pcg33_sell<4>;
+      if (sell_h == 4 && !launched) {
+        // full sliced-ELL copy, per-warp plan cache in shared memory
+        sell_build(c, 4);
+        SellDev sl = sell_dev(c);
+        void* kern = (void*)k_pcg33_stream<SellPhaseA>;
         const int wpb = kTB / 32;
         for (int per = kSpmvMinB; per >= 1 && !launched; --per) {
           int gsz = per * sm_count();
@@ -1111,7 +1138,12 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
           if (occ < per) continue;
           c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
           double* part = c.partials.p;
-          void* args[] = {&sl, &nb, &K, &TW, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
+          SellPhaseA A{};
+          A.SL = sl;
+          A.nb = nb;
+          A.K = K;
+          A.TW = TW;
+          void* args[] = {&A, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
           YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, smem, s));
           launched = true;
         }
