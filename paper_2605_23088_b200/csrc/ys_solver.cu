@@ -501,6 +501,26 @@ __device__ __forceinline__ void grid_sync_counter(unsigned long long* count, uns
   __syncthreads();
 }
 
+// The counter barrier split in two: arrive (every thread's prior writes
+// ordered before the CTA's release-add) and wait (acquire poll), so a CTA can
+// issue loads that do not depend on other CTAs' writes in between.
+__device__ __forceinline__ void grid_arrive(unsigned long long* count) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+}
+
+__device__ __forceinline__ void grid_wait(unsigned long long* count, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
 // Fixed-order sum of n partials (stride between the K arrays = n) inside every CTA.
 template <int K>
 __device__ __forceinline__ void reduce_partials_all(const double* part, int n, double (&out)[K]) {
@@ -709,6 +729,8 @@ __global__ void __launch_bounds__(TB, MINB) k_pcg33_persistent(SpmvDev S0, SpmvD
 // (independent loads; a shared-memory row state with the slice mapping was
 // measured slower: its per-row chains are latency-bound).  Fixed-order
 // reductions (deterministic).
+__device__ __forceinline__ void prefetch_l2(const void* q) { asm volatile("prefetch.global.L2 [%0];" ::"l"(q)); }
+
 struct SellPhaseA {
   SellDev SL;
   int64_t nb;
@@ -769,6 +791,43 @@ struct SellPhaseA {
   }
 };
 
+// Phase-B rows of one thread: b0 = global thread id, b0 + threads, ...  The
+// operands of the first row (p, r, x, M^-1 — none written in phase A) are
+// prefetched into L2 between the barrier's arrive and wait.
+
+struct RowRegs {
+  double p[3], r[3], x[3], M[9], z[3];
+};
+
+__device__ __forceinline__ void rowregs_load(RowRegs& q, int64_t b, const double* __restrict__ p,
+                                             const double* __restrict__ r, const double* __restrict__ x,
+                                             const double* __restrict__ minv) {
+  load_vec3(p + 3 * b, q.p[0], q.p[1], q.p[2]);
+  load_vec3(r + 3 * b, q.r[0], q.r[1], q.r[2]);
+  load_vec3(x + 3 * b, q.x[0], q.x[1], q.x[2]);
+  load_block9(minv + 9 * b, q.M);
+}
+
+// x += a p, r -= a hp, z = M^-1 r (stores x, r; z stays in q), r.r / r.z partials
+__device__ __forceinline__ void rowregs_update(RowRegs& q, int64_t b, double alpha, const double* hp, double* x,
+                                               double* r, double (&v)[2]) {
+  double hh[3];
+  load_vec3_cg(hp + 3 * b, hh[0], hh[1], hh[2]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    q.x[i] += alpha * q.p[i];
+    q.r[i] -= alpha * hh[i];
+  }
+  precond_apply<3>(q.M, q.r, q.z);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    x[3 * b + i] = q.x[i];
+    r[3 * b + i] = q.r[i];
+    v[0] += q.r[i] * q.r[i];
+    v[1] += q.r[i] * q.z[i];
+  }
+}
+
 template <class PA>
 __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t nb, const double* __restrict__ minv,
                                                                double* __restrict__ x, double* __restrict__ r,
@@ -778,6 +837,9 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
   extern __shared__ double smem[];
   const int G = gridDim.x;
   A.prologue(smem);
+  const int64_t nth = int64_t(G) * blockDim.x;
+  const int64_t b0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool has0 = b0 < nb;
   const double gnorm = st->gnorm;
   const double tol = st->tol;
   const long long max_iter = st->max_iter;
@@ -788,13 +850,23 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
   double rel = st->rel, php = 0.0, alpha = 0.0;
   unsigned long long ph[4] = {0, 0, 0, 0};
   unsigned long long epoch = 0;
+  unsigned long long* cnt = &gb->arrivals;
   unsigned long long t0 = gtimer();
   while (status == 0) {
     // ---- phase A: hp = H p, pHp partials
     double dot[1] = {A.run(p, hp)};
     block_reduce<1>(dot);
     if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
-    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    grid_arrive(cnt);
+    // phase B operands that no CTA writes in phase A: pulled into L2 under the barrier
+    if (has0) {
+      prefetch_l2(p + 3 * b0);
+      prefetch_l2(r + 3 * b0);
+      prefetch_l2(x + 3 * b0);
+      prefetch_l2(minv + 9 * b0);
+      prefetch_l2(minv + 9 * b0 + 8);
+    }
+    grid_wait(cnt, (unsigned long long)G * ++epoch);
     unsigned long long t1 = gtimer();
     ph[0] += t1 - t0;
     t0 = t1;
@@ -808,35 +880,20 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
     alpha = rz / php;
     // ---- phase B: x += a p, r -= a hp, z = M^-1 r, partials of r.r and r.z
     double v[2] = {0.0, 0.0};
-    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(G) * blockDim.x) {
-      const int64_t s0 = 3 * b;
-      double pp[3], hh[3], rr[3], xx[3], zz[3], M[9];
-      load_vec3(p + s0, pp[0], pp[1], pp[2]);
-      load_vec3_cg(hp + s0, hh[0], hh[1], hh[2]);
-      load_vec3(r + s0, rr[0], rr[1], rr[2]);
-      load_vec3(x + s0, xx[0], xx[1], xx[2]);
-      load_block9(minv + 9 * b, M);
+    for (int64_t b = b0; b < nb; b += nth) {
+      RowRegs q;
+      rowregs_load(q, b, p, r, x, minv);
+      rowregs_update(q, b, alpha, hp, x, r, v);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        xx[i] += alpha * pp[i];
-        rr[i] -= alpha * hh[i];
-      }
-      precond_apply<3>(M, rr, zz);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        x[s0 + i] = xx[i];
-        r[s0 + i] = rr[i];
-        z[s0 + i] = zz[i];
-        v[0] += rr[i] * rr[i];
-        v[1] += rr[i] * zz[i];
-      }
+      for (int i = 0; i < 3; ++i) z[3 * b + i] = q.z[i];
     }
     block_reduce<2>(v);
     if (threadIdx.x == 0) {
       part[G + blockIdx.x] = v[0];
       part[2 * G + blockIdx.x] = v[1];
     }
-    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    grid_arrive(cnt);
+    grid_wait(cnt, (unsigned long long)G * ++epoch);
     t1 = gtimer();
     ph[1] += t1 - t0;
     t0 = t1;
@@ -862,21 +919,16 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
     }
     const double beta = tot2[1] / rz;
     rz = tot2[1];
-    // ---- phase C: p = z + beta p
-    {
-      const int64_t n2 = (3 * nb) >> 1;
-      const double2* z2 = reinterpret_cast<const double2*>(z);
-      double2* p2 = reinterpret_cast<double2*>(p);
-      for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2; i += int64_t(G) * blockDim.x) {
-        const double2 zz = __ldcg(z2 + i);
-        double2 q = p2[i];
-        q.x = zz.x + beta * q.x;
-        q.y = zz.y + beta * q.y;
-        p2[i] = q;
-      }
-      if (((3 * nb) & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[3 * nb - 1] = z[3 * nb - 1] + beta * p[3 * nb - 1];
+    // ---- phase C: p = z + beta p (this thread's own rows: z is its own write)
+    for (int64_t b = b0; b < nb; b += nth) {
+      double zz[3], pp[3];
+      load_vec3(z + 3 * b, zz[0], zz[1], zz[2]);
+      load_vec3(p + 3 * b, pp[0], pp[1], pp[2]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) p[3 * b + i] = zz[i] + beta * pp[i];
     }
-    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    grid_arrive(cnt);
+    grid_wait(cnt, (unsigned long long)G * ++epoch);
     t1 = gtimer();
     ph[3] += t1 - t0;
     t0 = t1;
