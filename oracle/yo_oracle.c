@@ -27,7 +27,10 @@
  * (oracle/_ref, see oracle/Makefile).
  */
 #include <math.h>
+#include <pthread.h>
 #include <setjmp.h>
+#include <stdatomic.h>
+#include <unistd.h>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -166,10 +169,25 @@ struct yo_context {
   int64_t dist_bounds[65], dist_exp_off[65];
 };
 
-/* ------------------------------------------------------------------------ */
+/* ------------------------------------------------------------------------
+ * Errors.  Inside the parallel local-evaluation phase (the reference's
+ * parallel_for over instances, assembly.cpp:334-336) a failing instance
+ * records its error and unwinds to its own thread-local jump buffer; the
+ * serial phase then reports the failure of the lowest instance index, as the
+ * serial loop would. */
+static _Thread_local jmp_buf* TL_JB;
+static _Thread_local int TL_CLS;
+static _Thread_local char TL_MSG[256];
+
 static void fail(yo_context* c, int cls, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
+  if (TL_JB) {
+    vsnprintf(TL_MSG, sizeof(TL_MSG), fmt, ap);
+    va_end(ap);
+    TL_CLS = cls;
+    longjmp(*TL_JB, 1);
+  }
   vsnprintf(c->err, sizeof(c->err), fmt, ap);
   va_end(ap);
   c->err_cls = cls;
@@ -195,8 +213,8 @@ typedef struct {
   double h[MAXW * MAXW];
 } Jet;
 
-static int JN; /* active dimension */
-static yo_context* JC; /* for errors */
+static _Thread_local int JN;          /* active dimension */
+static _Thread_local yo_context* JC;  /* for errors */
 
 static void j_const(Jet* o, double v) {
   o->v = v;
@@ -849,114 +867,194 @@ static void diag_add(yo_context* c, int64_t gstart, const double* b, int len) {
   for (int k = 0; k < len * len; ++k) d[k] += b[k];
 }
 
+/* One instance's local gradient (width) and compressed, symmetrised,
+ * projected Hessian (m x m): assemble_local (assembly.cpp:284-321). */
+static void local_assemble(yo_context* c, const Energy* e, int64_t i, int project, int with_h, Jet* E, double* g,
+                           double* hc) {
+  const Slot* s = e->slots + i * e->kappa;
+  const Plan* p = &e->plans[i];
+  const int m = p->m;
+  const int reduced = e->mode == YS_PROJECT_REDUCED && e->kind == K_SNH;
+  if (!reduced) {
+    JN = e->width;
+    JC = c;
+    local_eval(c, e, i, c->X, E);
+    for (int k = 0; k < e->width; ++k) g[k] = E->g[k];
+    if (!with_h) return;
+    /* local_compress (assembly.cpp:266-282) */
+    for (int k = 0; k < m * m; ++k) hc[k] = 0.0;
+    for (int a = 0; a < e->kappa; ++a) {
+      const int us = p->slot2ub[a];
+      if (us < 0) continue;
+      for (int b = 0; b < e->kappa; ++b) {
+        const int ut = p->slot2ub[b];
+        if (ut < 0) continue;
+        for (int r = 0; r < s[a].len; ++r)
+          for (int q = 0; q < s[b].len; ++q)
+            hc[(p->ub[us].comp_col + r) * m + p->ub[ut].comp_col + q] += E->h[(s[a].col + r) * e->width + s[b].col + q];
+      }
+    }
+    /* 0.5 (H + H^T), then psd_project */
+    double sym[MAXW * MAXW];
+    for (int r = 0; r < m; ++r)
+      for (int q = 0; q < m; ++q) sym[r * m + q] = 0.5 * (hc[r * m + q] + hc[q * m + r]);
+    memcpy(hc, sym, sizeof(double) * m * m);
+    if (project && m > 0) psd_project(hc, m);
+    return;
+  }
+  /* ReducedProject: inner variable vec_rm(F) (9), J = dF/dx (9 x 12) */
+  JN = 9;
+  JC = c;
+  Jet F[9];
+  double x[12];
+  for (int l = 0; l < 4; ++l)
+    for (int k = 0; k < 3; ++k) x[3 * l + k] = c->X[c->t[e->target].start + 3 * e->conn[4 * i + l] + k];
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) j_var(&F[3 * r + cc], x[3 * (cc + 1) + r] - x[r], 3 * r + cc);
+  snh_psi(e, i, F, E);
+  double J[9 * 12];
+  memset(J, 0, sizeof(J));
+  for (int r = 0; r < 3; ++r)
+    for (int cc = 0; cc < 3; ++cc) {
+      J[(3 * r + cc) * 12 + 3 * (cc + 1) + r] = 1.0;
+      J[(3 * r + cc) * 12 + r] = -1.0;
+    }
+  for (int k = 0; k < 12; ++k) {
+    double acc = 0.0;
+    for (int q = 0; q < 9; ++q) acc += E->g[q] * J[q * 12 + k];
+    g[k] = acc;
+  }
+  if (!with_h) return;
+  double hin[81];
+  for (int r = 0; r < 9; ++r)
+    for (int q = 0; q < 9; ++q) hin[r * 9 + q] = 0.5 * (E->h[r * 9 + q] + E->h[q * 9 + r]);
+  if (project) psd_project(hin, 9);
+  double jc[9 * MAXW];
+  memset(jc, 0, sizeof(jc));
+  for (int a = 0; a < e->kappa; ++a) {
+    const int us = p->slot2ub[a];
+    if (us < 0) continue;
+    for (int q = 0; q < 9; ++q)
+      for (int r = 0; r < s[a].len; ++r) jc[q * m + p->ub[us].comp_col + r] += J[q * 12 + s[a].col + r];
+  }
+  for (int r = 0; r < m; ++r)
+    for (int q = 0; q < m; ++q) {
+      double acc = 0.0;
+      for (int a = 0; a < 9; ++a)
+        for (int b = 0; b < 9; ++b) acc += jc[a * m + r] * hin[a * 9 + b] * jc[b * m + q];
+      hc[r * m + q] = acc;
+    }
+}
+
+/* Instance loop of assemble_group (assembly.cpp:323-374): local results of a
+ * chunk of instances in parallel (host threads, dynamic blocks of 64; each
+ * instance is independent, so the results are those of the serial loop bit
+ * for bit), then the scatter serially in instance order.  YO_THREADS caps the
+ * thread count (default: all online CPUs). */
+#define CHUNK 32768
+typedef struct {
+  yo_context* c;
+  const Energy* e;
+  int64_t i0, n;
+  int project, with_h;
+  atomic_llong next;
+  double *gbuf, *hbuf;
+  int* ebuf;
+  char (*mbuf)[256];
+} LocalJob;
+
+static void* local_worker(void* arg) {
+  LocalJob* j = (LocalJob*)arg;
+  static _Thread_local Jet E;
+  for (;;) {
+    const int64_t k0 = atomic_fetch_add(&j->next, 64);
+    if (k0 >= j->n) break;
+    const int64_t k1 = k0 + 64 < j->n ? k0 + 64 : j->n;
+    for (int64_t k = k0; k < k1; ++k) {
+      jmp_buf jb;
+      j->ebuf[k] = 0;
+      if (setjmp(jb)) {
+        TL_JB = NULL;
+        j->ebuf[k] = TL_CLS;
+        memcpy(j->mbuf[k], TL_MSG, 256);
+        continue;
+      }
+      TL_JB = &jb;
+      local_assemble(j->c, j->e, j->i0 + k, j->project, j->with_h, &E, j->gbuf + k * MAXW,
+                     j->hbuf + k * MAXW * MAXW);
+      TL_JB = NULL;
+    }
+  }
+  return NULL;
+}
+
+static int host_threads(void) {
+  const char* v = getenv("YO_THREADS");
+  long n = v ? atol(v) : sysconf(_SC_NPROCESSORS_ONLN);
+  return n < 1 ? 1 : n > 256 ? 256 : (int)n;
+}
+
 static void assemble_group(yo_context* c, int which, int project, int with_h) {
-  static Jet E;
-  double hc[MAXW * MAXW];
+  double* gbuf = (double*)xcalloc((size_t)CHUNK * MAXW, sizeof(double));
+  double* hbuf = (double*)xcalloc((size_t)CHUNK * MAXW * MAXW, sizeof(double));
+  int* ebuf = (int*)xcalloc(CHUNK, sizeof(int));
+  char(*mbuf)[256] = calloc(CHUNK, 256);
+  const int nt = host_threads();
+  pthread_t th[256];
   for (int ei = 0; ei < c->ne; ++ei) {
     Energy* e = &c->e[ei];
     if (e->dynamic != which || e->n == 0 || e->kappa == 0) continue;
-    if (e->nplans != energy_count(c, e))
+    if (e->nplans != energy_count(c, e)) {
+      free(gbuf), free(hbuf), free(ebuf), free(mbuf);
       fail(c, YS_ERR_VALIDATION, "energy '%d': instance plans are stale; rebuild the dynamic structures", ei);
-    const int reduced = e->mode == YS_PROJECT_REDUCED && e->kind == K_SNH;
-    for (int64_t i = 0; i < e->n; ++i) {
-      const Slot* s = e->slots + i * e->kappa;
-      const Plan* p = &e->plans[i];
-      double g[MAXW];
-      const int m = p->m;
-      if (!reduced) {
-        JN = e->width;
-        JC = c;
-        local_eval(c, e, i, c->X, &E);
-        for (int k = 0; k < e->width; ++k) g[k] = E.g[k];
-        if (with_h) {
-          /* local_compress (assembly.cpp:266-282) */
-          for (int k = 0; k < m * m; ++k) hc[k] = 0.0;
-          for (int a = 0; a < e->kappa; ++a) {
-            const int us = p->slot2ub[a];
-            if (us < 0) continue;
-            for (int b = 0; b < e->kappa; ++b) {
-              const int ut = p->slot2ub[b];
-              if (ut < 0) continue;
-              for (int r = 0; r < s[a].len; ++r)
-                for (int q = 0; q < s[b].len; ++q)
-                  hc[(p->ub[us].comp_col + r) * m + p->ub[ut].comp_col + q] +=
-                      E.h[(s[a].col + r) * e->width + s[b].col + q];
-            }
-          }
-          /* 0.5 (H + H^T), then psd_project */
-          double sym[MAXW * MAXW];
-          for (int r = 0; r < m; ++r)
-            for (int q = 0; q < m; ++q) sym[r * m + q] = 0.5 * (hc[r * m + q] + hc[q * m + r]);
-          memcpy(hc, sym, sizeof(double) * m * m);
-          if (project && m > 0) psd_project(hc, m);
+    }
+    for (int64_t i0 = 0; i0 < e->n; i0 += CHUNK) {
+      const int64_t n = e->n - i0 < CHUNK ? e->n - i0 : CHUNK;
+      LocalJob job = {c, e, i0, n, project, with_h, 0, gbuf, hbuf, ebuf, mbuf};
+      atomic_init(&job.next, 0);
+      const int use = (int)(n / 256 + 1) < nt ? (int)(n / 256 + 1) : nt;
+      for (int t = 1; t < use; ++t) pthread_create(&th[t], NULL, local_worker, &job);
+      local_worker(&job);
+      for (int t = 1; t < use; ++t) pthread_join(th[t], NULL);
+      for (int64_t k = 0; k < n; ++k)
+        if (ebuf[k]) {
+          int cls = ebuf[k];
+          char msg[256];
+          memcpy(msg, mbuf[k], 256);
+          free(gbuf), free(hbuf), free(ebuf), free(mbuf);
+          fail(c, cls, "%s", msg);
         }
-      } else {
-        /* ReducedProject: inner variable vec_rm(F) (9), J = dF/dx (9 x 12) */
-        JN = 9;
-        JC = c;
-        Jet F[9];
-        double x[12];
-        for (int l = 0; l < 4; ++l)
-          for (int k = 0; k < 3; ++k) x[3 * l + k] = c->X[c->t[e->target].start + 3 * e->conn[4 * i + l] + k];
-        for (int r = 0; r < 3; ++r)
-          for (int cc = 0; cc < 3; ++cc) j_var(&F[3 * r + cc], x[3 * (cc + 1) + r] - x[r], 3 * r + cc);
-        snh_psi(e, i, F, &E);
-        double J[9 * 12];
-        memset(J, 0, sizeof(J));
-        for (int r = 0; r < 3; ++r)
-          for (int cc = 0; cc < 3; ++cc) {
-            J[(3 * r + cc) * 12 + 3 * (cc + 1) + r] = 1.0;
-            J[(3 * r + cc) * 12 + r] = -1.0;
-          }
-        for (int k = 0; k < 12; ++k) {
-          double acc = 0.0;
-          for (int q = 0; q < 9; ++q) acc += E.g[q] * J[q * 12 + k];
-          g[k] = acc;
-        }
-        if (with_h) {
-          double hin[81];
-          for (int r = 0; r < 9; ++r)
-            for (int q = 0; q < 9; ++q) hin[r * 9 + q] = 0.5 * (E.h[r * 9 + q] + E.h[q * 9 + r]);
-          if (project) psd_project(hin, 9);
-          double jc[9 * MAXW];
-          memset(jc, 0, sizeof(jc));
-          for (int a = 0; a < e->kappa; ++a) {
-            const int us = p->slot2ub[a];
-            if (us < 0) continue;
-            for (int q = 0; q < 9; ++q)
-              for (int r = 0; r < s[a].len; ++r) jc[q * m + p->ub[us].comp_col + r] += J[q * 12 + s[a].col + r];
-          }
-          for (int r = 0; r < m; ++r)
-            for (int q = 0; q < m; ++q) {
-              double acc = 0.0;
-              for (int a = 0; a < 9; ++a)
-                for (int b = 0; b < 9; ++b) acc += jc[a * m + r] * hin[a * 9 + b] * jc[b * m + q];
-              hc[r * m + q] = acc;
-            }
-        }
-      }
       /* scatter in instance order (assembly.cpp:346-372) */
-      for (int a = 0; a < e->kappa; ++a) {
-        if (s[a].index == 0) continue;
-        for (int r = 0; r < s[a].len; ++r) c->G[s[a].index - 1 + r] += g[s[a].col + r];
-      }
-      if (!with_h) continue;
-      for (int d = 0; d < p->nd; ++d) {
-        const UBlock* lo = &p->ub[p->d[d].ua];
-        const UBlock* hi = &p->ub[p->d[d].ub];
-        double* dst = c->H[which].values + p->d[d].value_offset;
-        for (int r = 0; r < lo->len; ++r)
-          for (int q = 0; q < hi->len; ++q) dst[r * hi->len + q] += hc[(lo->comp_col + r) * m + hi->comp_col + q];
-      }
-      for (int u = 0; u < p->nu; ++u) {
-        double b[81];
-        const UBlock* ub = &p->ub[u];
-        for (int r = 0; r < ub->len; ++r)
-          for (int q = 0; q < ub->len; ++q) b[r * ub->len + q] = hc[(ub->comp_col + r) * m + ub->comp_col + q];
-        diag_add(c, ub->gstart, b, ub->len);
+      for (int64_t k = 0; k < n; ++k) {
+        const int64_t i = i0 + k;
+        const Slot* s = e->slots + i * e->kappa;
+        const Plan* p = &e->plans[i];
+        const int m = p->m;
+        const double* g = gbuf + k * MAXW;
+        const double* hc = hbuf + k * MAXW * MAXW;
+        for (int a = 0; a < e->kappa; ++a) {
+          if (s[a].index == 0) continue;
+          for (int r = 0; r < s[a].len; ++r) c->G[s[a].index - 1 + r] += g[s[a].col + r];
+        }
+        if (!with_h) continue;
+        for (int d = 0; d < p->nd; ++d) {
+          const UBlock* lo = &p->ub[p->d[d].ua];
+          const UBlock* hi = &p->ub[p->d[d].ub];
+          double* dst = c->H[which].values + p->d[d].value_offset;
+          for (int r = 0; r < lo->len; ++r)
+            for (int q = 0; q < hi->len; ++q) dst[r * hi->len + q] += hc[(lo->comp_col + r) * m + hi->comp_col + q];
+        }
+        for (int u = 0; u < p->nu; ++u) {
+          double b[81];
+          const UBlock* ub = &p->ub[u];
+          for (int r = 0; r < ub->len; ++r)
+            for (int q = 0; q < ub->len; ++q) b[r * ub->len + q] = hc[(ub->comp_col + r) * m + ub->comp_col + q];
+          diag_add(c, ub->gstart, b, ub->len);
+        }
       }
     }
   }
+  free(gbuf), free(hbuf), free(ebuf), free(mbuf);
 }
 
 static void assemble(yo_context* c, int project, int with_h) {
@@ -972,27 +1070,72 @@ static void assemble(yo_context* c, int project, int with_h) {
 /* ------------------------------------------------------------------------
  * Solver (solver.cpp)
  * ------------------------------------------------------------------------ */
+static void spmv_range(const Bsr* h, const Group* g, int64_t k0, int64_t k1, const double* x, double* y) {
+  const int R = (int)g->rows, Cc = (int)g->cols;
+  for (int64_t k = k0; k < k1; ++k) {
+    const int64_t bi = g->coord_start + k;
+    const double* b = h->values + h->voff[bi];
+    const int64_t r = h->row[bi], cc = h->col[bi];
+    for (int i = 0; i < R; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < Cc; ++j) acc += b[i * Cc + j] * x[cc + j];
+      y[r + i] += acc;
+    }
+    if (r != cc)
+      for (int j = 0; j < Cc; ++j) {
+        double acc = 0.0;
+        for (int i = 0; i < R; ++i) acc += b[i * Cc + j] * x[r + i];
+        y[cc + j] += acc;
+      }
+  }
+}
+
+typedef struct {
+  const Bsr* h;
+  const Group* g;
+  int64_t k0, k1;
+  const double* x;
+  double* y;
+} SpmvShard;
+
+static void* spmv_shard(void* a) {
+  SpmvShard* s = (SpmvShard*)a;
+  spmv_range(s->h, s->g, s->k0, s->k1, s->x, s->y);
+  return NULL;
+}
+
+/* spmv_add (solver.cpp:59-82).  YO_SPMV_THREADS > 1 (the reference's
+ * "threads" > 1) with >= 1024 blocks: per group, block shards into per-thread
+ * partial vectors, reduced in shard order — the reference's threaded rounding.
+ * Default 1: the serial, deterministic order (the parity checker's mode). */
 static void spmv_add(const Bsr* h, const double* x, double* y) {
+  const char* v = getenv("YO_SPMV_THREADS");
+  int nt = v ? atoi(v) : 1;
+  if (nt > 64) nt = 64;
+  if (nt <= 1 || h->nb < 1024) {
+    for (int gi = 0; gi < h->ng; ++gi) spmv_range(h, &h->groups[gi], 0, h->groups[gi].count, x, y);
+    return;
+  }
+  const int64_t n = h->s;
+  double* part = (double*)xcalloc((size_t)nt * (size_t)n, sizeof(double));
+  pthread_t th[64];
+  SpmvShard sh[64];
   for (int gi = 0; gi < h->ng; ++gi) {
     const Group* g = &h->groups[gi];
-    const int R = (int)g->rows, Cc = (int)g->cols;
-    for (int64_t k = 0; k < g->count; ++k) {
-      const int64_t bi = g->coord_start + k;
-      const double* b = h->values + h->voff[bi];
-      const int64_t r = h->row[bi], cc = h->col[bi];
-      for (int i = 0; i < R; ++i) {
-        double acc = 0.0;
-        for (int j = 0; j < Cc; ++j) acc += b[i * Cc + j] * x[cc + j];
-        y[r + i] += acc;
-      }
-      if (r != cc)
-        for (int j = 0; j < Cc; ++j) {
-          double acc = 0.0;
-          for (int i = 0; i < R; ++i) acc += b[i * Cc + j] * x[r + i];
-          y[cc + j] += acc;
-        }
+    const int64_t per = (g->count + nt - 1) / nt;
+    int used = 0;
+    for (int t = 0; t < nt; ++t) {
+      const int64_t b = t * per, e = b + per < g->count ? b + per : g->count;
+      if (b >= e) break;
+      sh[t] = (SpmvShard){h, g, b, e, x, part + (size_t)t * (size_t)n};
+      pthread_create(&th[t], NULL, spmv_shard, &sh[t]);
+      ++used;
     }
+    for (int t = 0; t < used; ++t) pthread_join(th[t], NULL);
   }
+  for (int t = 0; t < nt; ++t)
+    for (int64_t i = 0; i < n; ++i) y[i] += part[(size_t)t * (size_t)n + (size_t)i];
+  free(part);
 }
 
 /* Eigen dynamic inverse() = PartialPivLU (solver.cpp:107) */
