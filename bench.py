@@ -333,7 +333,7 @@ def main():
                    "nh_via_deformation_gradient": bool(args.via_f),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
                    "parallelism": f"pcg-rows{world} (eval/assembly replicated)" if world > 1 else "single"},
-        "roofline": {"kernel": "k_pcg33_sell<4> (whole PCG solve incl. the sliced-ELL repack, one cooperative launch)" if world == 1 else
+        "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else
                      "row-partitioned PCG (k_dspmv33 / k_dupdate per rank + NCCL allgather)",
                      "bound": "hbm", "achieved": pcg_gbs, "peak": peak, "unit": "GB/s", "frac": pcg_gbs / peak,
                      "traffic": traffic_from_profiles(args.config, "pcg_dram_bytes_per_iteration"),

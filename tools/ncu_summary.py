@@ -39,7 +39,7 @@ for r in rows[1:]:
     total += t
 lines = [f"# {tag}: kernel launch list of `python bench.py --config {scene} --steps 2 --warmup 1 --no-cpu-baseline`",
          "under `ncu --metrics gpu__time_duration.sum --clock-control none`.  The uniform-3x3 PCG is one",
-         "cooperative launch per solve (`k_pcg33_sell`); the bench's own kernel-timing hooks",
+         "cooperative launch per solve (`k_pcg33_stream`); the bench's own kernel-timing hooks",
          "(`ys_time_kernel`: SpMV x50, assembly x10, eval x5) run after the timed steps and appear here too.",
          "Per-launch times are cold-cache and serialised; compare shares, not absolutes.", "",
          "| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
@@ -98,7 +98,7 @@ prev = d.get(scene, {})
 d[scene] = dict(prev, tag=tag, kernels=summary)
 if sp:
     d[scene]["spmv_dram_bytes"] = 1e6 * (sp[0]["dram__bytes_read.sum"] + sp[0]["dram__bytes_write.sum"])
-pp = [v for k, v in summary.items() if base(k).startswith("k_pcg33_sell")] or \
+pp = [v for k, v in summary.items() if base(k).startswith("k_pcg33_stream") or base(k).startswith("k_pcg33_sell")] or \
      [v for k, v in summary.items() if base(k).startswith("k_pcg33_persistent")]
 if pp and pcg_iters:
     d[scene]["pcg_iterations"] = pcg_iters
