@@ -217,6 +217,7 @@ struct Context {
   DevBuf<int> sell_tw;  // max entry rows per warp (persistent PCG plan cache)
   int sell_h = 0;
   int64_t sell_rows = 0, sell_slices = 0;  // entry rows, slices
+  int64_t sell_r0 = 0, sell_r1 = 0;         // block-row range of the copy
 
   // structure-build scratch (reused across dynamic rebuilds)
   DevBuf<unsigned char> cubtmp;
@@ -286,7 +287,7 @@ void spmv_structure(Context& c, Structure& st, const BlocksDev& blocks, const do
 
 BlocksDev blocks_view(Context& c);
 void drop_pcg_graph(Context& c);
-void sell_build(Context& c, int lanes_per_row);  // ys_sell.cu
+void sell_build(Context& c, int lanes_per_row, int64_t r0 = 0, int64_t r1 = -1);  // ys_sell.cu
 void spmv_sell(Context& c, const double* x, double* y);
 int sell_max_warp_rows(Context& c, int64_t warps, int slices_per_warp);   // y = H x through the sliced-ELL copy
 bool pcg_uses_conditional_graph(Context& c);

@@ -27,13 +27,14 @@ __device__ __forceinline__ int row_entries(const SpmvDev& S, int64_t R) {
   return (S.nrow[R + 1] - S.nrow[R]) + (S.trow[R + 1] - S.trow[R]);
 }
 
-__global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, int32_t* len) {
-  const int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (R >= nb) return;
-  len[R] = row_entries(S0, R) + (has1 ? row_entries(S1, R) : 0);
+__global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1, int32_t* len) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r0 + q >= r1) return;
+  len[q] = row_entries(S0, r0 + q) + (has1 ? row_entries(S1, r0 + q) : 0);
 }
 
-// width of slice s (in entry rows) = max over its rows of ceil(len / H)
+// width of slice s (in entry rows) = max over its rows of ceil(len / H); len and
+// nb relative to the range
 __global__ void k_sell_width(const int32_t* len, int64_t nb, int H, int64_t nslices, int64_t* width) {
   const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= nslices) return;
@@ -52,13 +53,15 @@ struct SellOut {
   int32_t* col;
   double* val;
   int H;
+  int64_t r0;
 };
 
 __device__ __forceinline__ void put_entry(const SellOut& o, int64_t R, int k, int32_t xcol, const double* __restrict__ b,
                                           bool transpose) {
   const int rps = 32 / o.H;
-  const int64_t slice = R / rps;
-  const int lane = int(R % rps) * o.H + k % o.H;
+  const int64_t q = R - o.r0;
+  const int64_t slice = q / rps;
+  const int lane = int(q % rps) * o.H + k % o.H;
   const int64_t e = o.soff[slice] + k / o.H;
   o.col[e * 32 + lane] = xcol;
   double v[9];
@@ -83,9 +86,9 @@ __device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int
 
 // One thread per block row; the threads of a slice write the same entry row
 // together (coalesced stores).
-__global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t nb, SellOut o) {
-  const int64_t R = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (R >= nb) return;
+__global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t r1, SellOut o) {
+  const int64_t R = o.r0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (R >= r1) return;
   int k = fill_from(S0, o, R, 0);
   if (has1) fill_from(S1, o, R, k);
 }
@@ -139,21 +142,24 @@ int sell_max_warp_rows(Context& c, int64_t NW, int K) {
 }
 
 SellDev sell_dev(Context& c) {
-  return SellDev{c.sell_len.p, c.sell_soff.p, c.sell_col.p, c.sell_val.p, c.NB, c.sell_slices};
+  return SellDev{c.sell_len.p, c.sell_soff.p, c.sell_col.p, c.sell_val.p, c.sell_r1, c.sell_slices, c.sell_r0};
 }
 
 // Builds the sliced-ELL copy of S[0] + S[1] (uniform 3x3 systems only) with H
-// lanes per block row.  One host synchronisation (the entry-row count sizes
+// lanes per block row, over the block rows [r0, r1) (r1 < 0: all rows).  One host synchronisation (the entry-row count sizes
 // the buffers).
-void sell_build(Context& c, int H) {
+void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   cudaStream_t s = c.stream;
   const bool has1 = c.S[1].n_blocks > 0;
   SpmvDev d0 = spmv_dev(c.S[0]);
   SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
-  const int64_t nb = c.NB;
+  if (r1 < 0) r1 = c.NB;
+  const int64_t nb = r1 - r0;
   const int rps = 32 / H;
   const int64_t nsl = ceil_div(nb, rps);
   c.sell_h = H;
+  c.sell_r0 = r0;
+  c.sell_r1 = r1;
   c.sell_slices = nsl;
   c.sell_len.resize(size_t(std::max<int64_t>(nb, 1)));
   c.sell_soff.resize(size_t(nsl + 1));
@@ -161,7 +167,7 @@ void sell_build(Context& c, int H) {
     c.sell_rows = 0;
     return;
   }
-  k_sell_len<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, nb, c.sell_len.p);
+  k_sell_len<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, r0, r1, c.sell_len.p);
   k_sell_width<<<int(ceil_div(nsl, kTB)), kTB, 0, s>>>(c.sell_len.p, nb, H, nsl, c.sell_soff.p);
   YS_LAUNCH_CHECK();
   int64_t* so = c.sell_soff.p;
@@ -176,8 +182,8 @@ void sell_build(Context& c, int H) {
   c.sell_rows = rows;
   c.sell_col.resize(size_t(rows * 32 + 4));
   c.sell_val.resize(size_t(rows * 288 + 4));
-  k_sell_fill<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, nb,
-                                                     SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H});
+  k_sell_fill<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, r1,
+                                                     SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
   YS_LAUNCH_CHECK();
 }
 

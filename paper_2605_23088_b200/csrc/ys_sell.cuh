@@ -11,7 +11,8 @@
 // values change every iteration, the PCG then runs hundreds of SpMVs) into a
 // full (both-triangle) sliced-ELL layout:
 //   * a slice is 32 lanes = 32/H block rows, H lanes per row; entry k of row R
-//     goes to lane (R mod 32/H)*H + k mod H, entry row k / H of the slice;
+//     goes to lane ((R - r0) mod 32/H)*H + k mod H, entry row k / H of the
+//     slice (r0: first row of the copy's range, 0 on one GPU);
 //   * an entry row of a slice is 32 int32 column DoFs and 32 x 72 B of values
 //     as [4][32] double2 + [32] double, so every load instruction of a warp is
 //     one contiguous 512 B (or 256 B) run: fully coalesced, no index chains;
@@ -31,8 +32,9 @@ struct SellDev {
   const int64_t* soff;  // nslices + 1: first entry row of each slice
   const int32_t* col;   // entry rows x 32: column DoF
   const double* val;    // entry rows x 288
-  int64_t nb;
+  int64_t nb;       // end of the row range (exclusive)
   int64_t nslices;
+  int64_t r0;       // first row of the range (0; the owned rows' start in the distributed solve)
 };
 
 SellDev sell_dev(Context& c);  // ys_sell.cu
@@ -42,9 +44,9 @@ template <int H>
 __device__ __forceinline__ void sell_acc(const SellDev& S, int64_t slice, int lane, const double* x, double& a0,
                                          double& a1, double& a2, int64_t& R) {
   constexpr int RPS = 32 / H;
-  R = slice * RPS + lane / H;
+  R = S.r0 + slice * RPS + lane / H;
   const int h = lane % H;
-  const int L = R < S.nb ? S.len[R] : 0;
+  const int L = R < S.nb ? S.len[R - S.r0] : 0;
   const int Lh = L > h ? (L - h + H - 1) / H : 0;
   const int64_t e0 = S.soff[slice];
   for (int k = 0; k < Lh; k += 2) {
