@@ -27,10 +27,21 @@ __device__ __forceinline__ int row_entries(const SpmvDev& S, int64_t R) {
   return (S.nrow[R + 1] - S.nrow[R]) + (S.trow[R + 1] - S.trow[R]);
 }
 
+// Row R's own blocks are sorted by column, so its diagonal block (if any) is
+// the first one of each group.
+__device__ __forceinline__ bool has_diag(const SpmvDev& S, int64_t R) {
+  return S.nrow[R + 1] > S.nrow[R] && S.col[S.nrow[R]] == 3 * int32_t(R);
+}
+
+// The dynamic group's diagonal block of a row is merged into the static one
+// (one entry, B_s + B_d): the contact rows lose one entry each.
 __global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1, int32_t* len) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r0 + q >= r1) return;
-  len[q] = row_entries(S0, r0 + q) + (has1 ? row_entries(S1, r0 + q) : 0);
+  const int64_t R = r0 + q;
+  if (R >= r1) return;
+  int n = row_entries(S0, R);
+  if (has1) n += row_entries(S1, R) - ((has_diag(S0, R) && has_diag(S1, R)) ? 1 : 0);
+  len[q] = n;
 }
 
 // width of slice s (in entry rows) = max over its rows of ceil(len / H); len and
@@ -57,7 +68,7 @@ struct SellOut {
 };
 
 __device__ __forceinline__ void put_entry(const SellOut& o, int64_t R, int k, int32_t xcol, const double* __restrict__ b,
-                                          bool transpose) {
+                                          bool transpose, const double* __restrict__ b2 = nullptr) {
   const int rps = 32 / o.H;
   const int64_t q = R - o.r0;
   const int64_t slice = q / rps;
@@ -69,14 +80,23 @@ __device__ __forceinline__ void put_entry(const SellOut& o, int64_t R, int k, in
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) v[3 * i + j] = transpose ? b[3 * j + i] : b[3 * i + j];
+  if (b2)
+#pragma unroll
+    for (int i = 0; i < 9; ++i) v[i] += b2[i];
   double* base = o.val + e * 288;
 #pragma unroll
   for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(base)[q * 32 + lane] = make_double2(v[2 * q], v[2 * q + 1]);
   base[256 + lane] = v[8];
 }
 
-__device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int64_t R, int k) {
-  for (int32_t u = S.nrow[R]; u < S.nrow[R + 1]; ++u) put_entry(o, R, k++, S.col[u], S.values + 9 * int64_t(u), false);
+// skip_diag: the row's diagonal block was merged into an earlier entry;
+// diag_add: dynamic diagonal block to merge into this group's diagonal block.
+__device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int64_t R, int k, bool skip_diag = false,
+                                         const double* diag_add = nullptr) {
+  for (int32_t u = S.nrow[R] + (skip_diag ? 1 : 0); u < S.nrow[R + 1]; ++u) {
+    const bool dg = u == S.nrow[R] && S.col[u] == 3 * int32_t(R);
+    put_entry(o, R, k++, S.col[u], S.values + 9 * int64_t(u), false, dg ? diag_add : nullptr);
+  }
   for (int32_t j = S.trow[R]; j < S.trow[R + 1]; ++j) {
     const int2 t = S.tlist[j];
     put_entry(o, R, k++, t.y, S.values + 9 * int64_t(t.x), true);
@@ -89,8 +109,9 @@ __device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int
 __global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t r1, SellOut o) {
   const int64_t R = o.r0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (R >= r1) return;
-  int k = fill_from(S0, o, R, 0);
-  if (has1) fill_from(S1, o, R, k);
+  const bool merge = has1 && has_diag(S0, R) && has_diag(S1, R);
+  int k = fill_from(S0, o, R, 0, false, merge ? S1.values + 9 * int64_t(S1.nrow[R]) : nullptr);
+  if (has1) fill_from(S1, o, R, k, merge);
 }
 
 // Standalone y = H x through the sliced-ELL copy (ys_time_kernel and

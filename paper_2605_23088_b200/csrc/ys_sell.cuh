@@ -17,9 +17,11 @@
 //     as [4][32] double2 + [32] double, so every load instruction of a warp is
 //     one contiguous 512 B (or 256 B) run: fully coalesced, no index chains;
 //   * transposed blocks are stored transposed: all entries are y += B x.
-// Entries of a row: static own blocks, static transposed, dynamic own,
-// dynamic transposed (the reference's static-then-dynamic order, summed per
-// lane then by a fixed xor butterfly: deterministic, bitwise reproducible).
+// Entries of a row: static own blocks (the dynamic group's diagonal block is
+// added into the static diagonal block: one entry, B_s + B_d), static
+// transposed, dynamic own, dynamic transposed (the reference's
+// static-then-dynamic order, summed per lane then by a fixed xor butterfly:
+// deterministic, bitwise reproducible).
 // Padding slots (k >= the lane's count) are never read.
 #pragma once
 
