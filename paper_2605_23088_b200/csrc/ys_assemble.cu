@@ -157,14 +157,16 @@ __global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const doubl
   }
   const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
   if (full) edge_to_projection_space(hd);
-  expand_vertex_blocks(hd, full, wr);  // exact when M is PD; pass B overwrites otherwise
-  if (!cholesky_pd9(hd)) {
-    const unsigned k = atomicAdd(count, 1u);
-    list[k] = int32_t(i);
-    double* m = mbuf + 45 * int64_t(k);
-#pragma unroll
-    for (int q = 0; q < 45; ++q) m[q] = hd[q];
+  if (cholesky_pd9(hd)) {
+    expand_vertex_blocks(hd, full, wr);  // M is PD: the projection is M itself
+    return;
   }
+  // indefinite: pass B projects M and writes the vertex blocks
+  const unsigned k = atomicAdd(count, 1u);
+  list[k] = int32_t(i);
+  double* m = mbuf + 45 * int64_t(k);
+#pragma unroll
+  for (int q = 0; q < 45; ++q) m[q] = hd[q];
 }
 
 // Pass B: Jacobi EVD + clamp + reconstruction for the compacted indefinite
