@@ -67,51 +67,66 @@ struct SellOut {
   int64_t r0;
 };
 
-__device__ __forceinline__ void put_entry(const SellOut& o, int64_t R, int k, int32_t xcol, const double* __restrict__ b,
-                                          bool transpose, const double* __restrict__ b2 = nullptr) {
-  const int rps = 32 / o.H;
-  const int64_t q = R - o.r0;
-  const int64_t slice = q / rps;
-  const int lane = int(q % rps) * o.H + k % o.H;
-  const int64_t e = o.soff[slice] + k / o.H;
-  o.col[e * 32 + lane] = xcol;
-  double v[9];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) v[3 * i + j] = transpose ? b[3 * j + i] : b[3 * i + j];
-  if (b2)
-#pragma unroll
-    for (int i = 0; i < 9; ++i) v[i] += b2[i];
-  double* base = o.val + e * 288;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(base)[q * 32 + lane] = make_double2(v[2 * q], v[2 * q + 1]);
-  base[256 + lane] = v[8];
-}
-
-// skip_diag: the row's diagonal block was merged into an earlier entry;
-// diag_add: dynamic diagonal block to merge into this group's diagonal block.
-__device__ __forceinline__ int fill_from(const SpmvDev& S, const SellOut& o, int64_t R, int k, bool skip_diag = false,
-                                         const double* diag_add = nullptr) {
-  for (int32_t u = S.nrow[R] + (skip_diag ? 1 : 0); u < S.nrow[R + 1]; ++u) {
-    const bool dg = u == S.nrow[R] && S.col[u] == 3 * int32_t(R);
-    put_entry(o, R, k++, S.col[u], S.values + 9 * int64_t(u), false, dg ? diag_add : nullptr);
-  }
-  for (int32_t j = S.trow[R]; j < S.trow[R + 1]; ++j) {
-    const int2 t = S.tlist[j];
-    put_entry(o, R, k++, t.y, S.values + 9 * int64_t(t.x), true);
-  }
-  return k;
-}
-
-// One thread per block row; the threads of a slice write the same entry row
-// together (coalesced stores).
-__global__ void k_sell_fill(SpmvDev S0, SpmvDev S1, int has1, int64_t r1, SellOut o) {
-  const int64_t R = o.r0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// One lane per (row, k mod H) of a slice: lane l fills the entries k = l mod H,
+// l mod H + H, ... of row l / H, i.e. exactly its own lane column of every
+// entry row of the slice — each store instruction of the warp covers whole
+// contiguous runs.  Entries of a row: static own (the dynamic diagonal block merged
+// into the static one), static transposed, dynamic own, dynamic transposed.
+__global__ void k_sell_fill_lanes(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1, int H, SellOut o) {
+  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t sl = gt >> 5;
+  const int lane = int(gt & 31);
+  const int rps = 32 / H;
+  const int64_t R = r0 + sl * rps + lane / H;
   if (R >= r1) return;
+  const int j = lane % H;
   const bool merge = has1 && has_diag(S0, R) && has_diag(S1, R);
-  int k = fill_from(S0, o, R, 0, false, merge ? S1.values + 9 * int64_t(S1.nrow[R]) : nullptr);
-  if (has1) fill_from(S1, o, R, k, merge);
+  // segments: S0 own, S0 transposed, S1 own (minus a merged diagonal), S1 transposed
+  const int32_t n0 = S0.nrow[R + 1] - S0.nrow[R], t0 = S0.trow[R + 1] - S0.trow[R];
+  const int32_t u1 = has1 ? S1.nrow[R] + (merge ? 1 : 0) : 0;
+  const int32_t n1 = has1 ? S1.nrow[R + 1] - u1 : 0, t1 = has1 ? S1.trow[R + 1] - S1.trow[R] : 0;
+  const int L = n0 + t0 + n1 + t1;
+  const int64_t e0 = o.soff[sl];
+  for (int k = j; k < L; k += H) {
+    int32_t xcol;
+    const double* b;
+    bool tr = false;
+    const double* b2 = nullptr;
+    if (k < n0) {
+      const int32_t u = S0.nrow[R] + k;
+      xcol = S0.col[u];
+      b = S0.values + 9 * int64_t(u);
+      if (k == 0 && merge) b2 = S1.values + 9 * int64_t(S1.nrow[R]);
+    } else if (k < n0 + t0) {
+      const int2 t = S0.tlist[S0.trow[R] + (k - n0)];
+      xcol = t.y;
+      b = S0.values + 9 * int64_t(t.x);
+      tr = true;
+    } else if (k < n0 + t0 + n1) {
+      const int32_t u = u1 + (k - n0 - t0);
+      xcol = S1.col[u];
+      b = S1.values + 9 * int64_t(u);
+    } else {
+      const int2 t = S1.tlist[S1.trow[R] + (k - n0 - t0 - n1)];
+      xcol = t.y;
+      b = S1.values + 9 * int64_t(t.x);
+      tr = true;
+    }
+    const int64_t e = e0 + k / H;
+    o.col[e * 32 + lane] = xcol;
+    double v[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj) v[3 * i + jj] = tr ? b[3 * jj + i] : b[3 * i + jj];
+    if (b2)
+#pragma unroll
+      for (int i = 0; i < 9; ++i) v[i] += b2[i];
+    double* base = o.val + e * 288;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(base)[q * 32 + lane] = make_double2(v[2 * q], v[2 * q + 1]);
+    base[256 + lane] = v[8];
+  }
 }
 
 // Standalone y = H x through the sliced-ELL copy (ys_time_kernel and
@@ -203,8 +218,8 @@ void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   c.sell_rows = rows;
   c.sell_col.resize(size_t(rows * 32 + 4));
   c.sell_val.resize(size_t(rows * 288 + 4));
-  k_sell_fill<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, r1,
-                                                     SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
+  k_sell_fill_lanes<<<int(ceil_div(nsl * 32, kTB)), kTB, 0, s>>>(
+      d0, d1, has1 ? 1 : 0, r0, r1, H, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
   YS_LAUNCH_CHECK();
 }
 
