@@ -215,6 +215,8 @@ struct Context {
   DevBuf<int64_t> sell_soff;
   DevBuf<double> sell_val;
   DevBuf<int> sell_tw;  // max entry rows per warp (persistent PCG plan cache)
+  int64_t sell_tw_nw = -1;  // grid (warps) sell_tw_host was computed for
+  int sell_tw_host = 0;
   int sell_h = 0;
   int64_t sell_rows = 0, sell_slices = 0;  // entry rows, slices
   int64_t sell_r0 = 0, sell_r1 = 0;         // block-row range of the copy

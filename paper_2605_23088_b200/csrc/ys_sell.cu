@@ -166,6 +166,7 @@ __global__ void k_warp_rows(const int64_t* soff, int64_t nslices, int64_t NW, in
 }  // namespace
 
 int sell_max_warp_rows(Context& c, int64_t NW, int K) {
+  if (NW == c.sell_tw_nw && K == int(ceil_div(c.sell_slices, NW))) return c.sell_tw_host;  // from sell_build
   cudaStream_t s = c.stream;
   c.sell_tw.resize(1);
   YS_CUDA(cudaMemsetAsync(c.sell_tw.p, 0, sizeof(int), s));
@@ -212,10 +213,22 @@ void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   YS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, so, so, n, s));
   c.cubtmp.resize(std::max<size_t>(bytes, 1));
   YS_CUDA(cub::DeviceScan::InclusiveSum(c.cubtmp.p, bytes, so, so, n, s));
+  // the persistent PCG's plan-cache size for its grid (3 CTAs of 8 warps per
+  // SM) comes back with the same synchronisation
+  const int64_t nw = int64_t(kSpmvMinB) * sm_count() * (kTB / 32);
+  const int kw = int(ceil_div(nsl, nw));
+  c.sell_tw.resize(1);
+  YS_CUDA(cudaMemsetAsync(c.sell_tw.p, 0, sizeof(int), s));
+  k_warp_rows<<<int(ceil_div(nw, kTB)), kTB, 0, s>>>(so, nsl, nw, kw, c.sell_tw.p);
+  YS_LAUNCH_CHECK();
   int64_t rows = 0;
+  int tw = 0;
   YS_CUDA(cudaMemcpyAsync(&rows, so + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  YS_CUDA(cudaMemcpyAsync(&tw, c.sell_tw.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   YS_CUDA(cudaStreamSynchronize(s));
   c.sell_rows = rows;
+  c.sell_tw_nw = nw;
+  c.sell_tw_host = tw;
   c.sell_col.resize(size_t(rows * 32 + 4));
   c.sell_val.resize(size_t(rows * 288 + 4));
   k_sell_fill_lanes<<<int(ceil_div(nsl * 32, kTB)), kTB, 0, s>>>(
