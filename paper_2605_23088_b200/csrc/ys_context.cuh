@@ -212,6 +212,7 @@ struct Context {
   DevBuf<int> errflag;
   // sliced-ELL full copy of H_static + H_dynamic for the uniform 3x3 PCG (ys_sell.cuh)
   DevBuf<int32_t> sell_len, sell_col;
+  DevBuf<int32_t> sell_perm, sell_lenq;  // position -> row (rows sorted by length per window), length by position
   DevBuf<int64_t> sell_soff;
   DevBuf<double> sell_val;
   DevBuf<int> sell_tw;  // max entry rows per warp (persistent PCG plan cache)

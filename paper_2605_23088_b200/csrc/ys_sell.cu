@@ -44,6 +44,25 @@ __global__ void k_sell_len(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t
   len[q] = n;
 }
 
+// perm / lenq: inside each window of kSellSigma positions the rows sorted by
+// entry count, descending (stable: ties keep the row order).
+__global__ void __launch_bounds__(kSellSigma) k_sell_sort_windows(const int32_t* len, int64_t r0, int64_t nb,
+                                                                  int32_t* perm, int32_t* lenq) {
+  using Sort = cub::BlockRadixSort<uint32_t, kSellSigma, 1, int32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  const int64_t q = int64_t(blockIdx.x) * kSellSigma + threadIdx.x;
+  const bool live = q < nb;
+  const int L = live ? len[q] : 0;
+  // key: 0..1023 = 1023 - len for live rows (longest first), 1024 for padding
+  uint32_t key[1] = {live ? uint32_t(1023 - min(L, 1023)) : 1024u};
+  int32_t val[1] = {int32_t(q)};
+  Sort(tmp).Sort(key, val, 0, 11);
+  if (live) {
+    perm[q] = int32_t(r0) + val[0];
+    lenq[q] = len[val[0]];
+  }
+}
+
 // width of slice s (in entry rows) = max over its rows of ceil(len / H); len and
 // nb relative to the range
 __global__ void k_sell_width(const int32_t* len, int64_t nb, int H, int64_t nslices, int64_t* width) {
@@ -72,13 +91,15 @@ struct SellOut {
 // entry row of the slice — each store instruction of the warp covers whole
 // contiguous runs.  Entries of a row: static own (the dynamic diagonal block merged
 // into the static one), static transposed, dynamic own, dynamic transposed.
-__global__ void k_sell_fill_lanes(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1, int H, SellOut o) {
+__global__ void k_sell_fill_lanes(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1, int H,
+                                  const int32_t* __restrict__ perm, SellOut o) {
   const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t sl = gt >> 5;
   const int lane = int(gt & 31);
   const int rps = 32 / H;
-  const int64_t R = r0 + sl * rps + lane / H;
-  if (R >= r1) return;
+  const int64_t q = sl * rps + lane / H;
+  if (r0 + q >= r1) return;
+  const int64_t R = perm[q];
   const int j = lane % H;
   const bool merge = has1 && has_diag(S0, R) && has_diag(S1, R);
   // segments: S0 own, S0 transposed, S1 own (minus a merged diagonal), S1 transposed
@@ -179,7 +200,8 @@ int sell_max_warp_rows(Context& c, int64_t NW, int K) {
 }
 
 SellDev sell_dev(Context& c) {
-  return SellDev{c.sell_len.p, c.sell_soff.p, c.sell_col.p, c.sell_val.p, c.sell_r1, c.sell_slices, c.sell_r0};
+  return SellDev{c.sell_lenq.p, c.sell_soff.p, c.sell_col.p, c.sell_val.p, c.sell_r1, c.sell_slices, c.sell_r0,
+                 c.sell_perm.p};
 }
 
 // Builds the sliced-ELL copy of S[0] + S[1] (uniform 3x3 systems only) with H
@@ -199,13 +221,17 @@ void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   c.sell_r1 = r1;
   c.sell_slices = nsl;
   c.sell_len.resize(size_t(std::max<int64_t>(nb, 1)));
+  c.sell_lenq.resize(size_t(std::max<int64_t>(nb, 1)));
+  c.sell_perm.resize(size_t(std::max<int64_t>(nb, 1)));
   c.sell_soff.resize(size_t(nsl + 1));
   if (nb == 0) {
     c.sell_rows = 0;
     return;
   }
   k_sell_len<<<int(ceil_div(nb, kTB)), kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, r0, r1, c.sell_len.p);
-  k_sell_width<<<int(ceil_div(nsl, kTB)), kTB, 0, s>>>(c.sell_len.p, nb, H, nsl, c.sell_soff.p);
+  k_sell_sort_windows<<<int(ceil_div(nb, kSellSigma)), kSellSigma, 0, s>>>(c.sell_len.p, r0, nb, c.sell_perm.p,
+                                                                           c.sell_lenq.p);
+  k_sell_width<<<int(ceil_div(nsl, kTB)), kTB, 0, s>>>(c.sell_lenq.p, nb, H, nsl, c.sell_soff.p);
   YS_LAUNCH_CHECK();
   int64_t* so = c.sell_soff.p;
   const int n = int(nsl + 1);
@@ -232,7 +258,7 @@ void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   c.sell_col.resize(size_t(rows * 32 + 4));
   c.sell_val.resize(size_t(rows * 288 + 4));
   k_sell_fill_lanes<<<int(ceil_div(nsl * 32, kTB)), kTB, 0, s>>>(
-      d0, d1, has1 ? 1 : 0, r0, r1, H, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
+      d0, d1, has1 ? 1 : 0, r0, r1, H, c.sell_perm.p, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
   YS_LAUNCH_CHECK();
 }
 

@@ -10,9 +10,12 @@
 // Here H = H_static + H_dynamic is repacked ONCE per Newton iteration (its
 // values change every iteration, the PCG then runs hundreds of SpMVs) into a
 // full (both-triangle) sliced-ELL layout:
-//   * a slice is 32 lanes = 32/H block rows, H lanes per row; entry k of row R
-//     goes to lane ((R - r0) mod 32/H)*H + k mod H, entry row k / H of the
-//     slice (r0: first row of the copy's range, 0 on one GPU);
+//   * rows are placed at positions q (row perm[q]): inside each window of
+//     kSellSigma positions they are sorted by entry count (descending, stable),
+//     so the long contact rows share slices instead of widening many
+//     (C5: mean slice width 5.1 -> 4.3 entry rows);
+//   * a slice is 32 lanes = 32/H positions, H lanes per row; entry k of the
+//     row at position q goes to lane (q mod 32/H)*H + k mod H, entry row k / H;
 //   * an entry row of a slice is 32 int32 column DoFs and 32 x 72 B of values
 //     as [4][32] double2 + [32] double, so every load instruction of a warp is
 //     one contiguous 512 B (or 256 B) run: fully coalesced, no index chains;
@@ -37,7 +40,18 @@ struct SellDev {
   int64_t nb;       // end of the row range (exclusive)
   int64_t nslices;
   int64_t r0;       // first row of the range (0; the owned rows' start in the distributed solve)
+  const int32_t* perm;  // position q -> block row: rows sorted by entry count inside windows of
+                        // kSellSigma positions (long contact rows share slices); len is by position
 };
+
+// 31 slices of 8 rows: coprime with the warp counts of the grid-stride slice
+// loops (multiples of 32), so the window position of a warp's slices rotates
+// and the long slices spread over the warps (a 256-row window sent every
+// window's longest slice to the same warps: phase A 43 -> 80 us).
+constexpr int kSellSigma = 248;
+
+// Block row at position q of the copy (q < nb - r0).
+__device__ __forceinline__ int64_t sell_row(const SellDev& S, int64_t q) { return S.perm[q]; }
 
 SellDev sell_dev(Context& c);  // ys_sell.cu
 
@@ -46,9 +60,11 @@ template <int H>
 __device__ __forceinline__ void sell_acc(const SellDev& S, int64_t slice, int lane, const double* x, double& a0,
                                          double& a1, double& a2, int64_t& R) {
   constexpr int RPS = 32 / H;
-  R = S.r0 + slice * RPS + lane / H;
+  const int64_t q = slice * RPS + lane / H;
+  const bool live = q < S.nb - S.r0;
+  R = live ? sell_row(S, q) : S.nb;
   const int h = lane % H;
-  const int L = R < S.nb ? S.len[R - S.r0] : 0;
+  const int L = live ? S.len[q] : 0;
   const int Lh = L > h ? (L - h + H - 1) / H : 0;
   const int64_t e0 = S.soff[slice];
   for (int k = 0; k < Lh; k += 2) {

@@ -759,8 +759,8 @@ struct SellPhaseA {
     for (int k = 0; k < kn; ++k) {
       const int64_t sl = gw + k * NW;
       const int64_t e0 = SL.soff[sl], e1 = SL.soff[sl + 1];
-      const int64_t R = SL.r0 + sl * RPS + grp;
-      const int L = R < nb ? SL.len[R - SL.r0] : 0;
+      const int64_t q = sl * RPS + grp;
+      const int L = q < SL.nb - SL.r0 ? SL.len[q] : 0;
       const int Lh = L > h ? (L - h + H - 1) / H : 0;
       if (wl == 0) meta[k] = make_int2(int(e0), off);
       lhs[k * 32 + wl] = Lh;
@@ -778,8 +778,9 @@ struct SellPhaseA {
       const int2 m = meta[k];
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
       sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2);
-      const int64_t R = SL.r0 + (gw + k * NW) * RPS + grp;
-      if (h == 0 && R < nb) {
+      const int64_t q = (gw + k * NW) * RPS + grp;
+      if (h == 0 && q < SL.nb - SL.r0) {
+        const int64_t R = sell_row(SL, q);
         double* yo = hp + 3 * R;
         yo[0] = a0;
         yo[1] = a1;
