@@ -13,7 +13,7 @@
 //   * rows are placed at positions q (row perm[q]): inside each window of
 //     kSellSigma positions they are sorted by entry count (descending, stable),
 //     so the long contact rows share slices instead of widening many
-//     (C5: mean slice width 5.1 -> 4.3 entry rows);
+//     (C5: mean slice width 5.1 -> ~4.4 entry rows);
 //   * a slice is 32 lanes = 32/H positions, H lanes per row; entry k of the
 //     row at position q goes to lane (q mod 32/H)*H + k mod H, entry row k / H;
 //   * an entry row of a slice is 32 int32 column DoFs and 32 x 72 B of values
@@ -44,11 +44,12 @@ struct SellDev {
                         // kSellSigma positions (long contact rows share slices); len is by position
 };
 
-// 31 slices of 8 rows: coprime with the warp counts of the grid-stride slice
-// loops (multiples of 32), so the window position of a warp's slices rotates
-// and the long slices spread over the warps (a 256-row window sent every
-// window's longest slice to the same warps: phase A 43 -> 80 us).
-constexpr int kSellSigma = 248;
+// 63 slices of 8 rows: nearly coprime with the warp counts of the grid-stride
+// slice loops (multiples of 32), so the window position of a warp's slices
+// rotates and the long slices spread over the warps (a 256-row window sent
+// every window's longest slice to the same warps: phase A 43 -> 80 us).
+// C5 phase A by window: 120 rows 43.2, 248 40.9, 504 40.0, 760 41.5, 1016 45.3 us.
+constexpr int kSellSigma = 504;
 
 // Block row at position q of the copy (q < nb - r0).
 __device__ __forceinline__ int64_t sell_row(const SellDev& S, int64_t q) { return S.perm[q]; }
