@@ -670,10 +670,13 @@ static void record(Context& c, int idx) {
   if (c.profiling) YS_CUDA(cudaEventRecord(c.ev[idx], c.stream));
 }
 
-void ctx_eval_all(Context& c, bool project, bool with_hessian) {
-  cudaStream_t s = c.stream;
+// only: -1 every energy, 0 the static group's, 1 the dynamic group's; s: the
+// stream to launch on (default: the context stream).  The pass-B counters are
+// zeroed by the call that evaluates the static group (the stencil energies).
+void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStream_t s) {
+  if (!s) s = c.stream;
   c.evd_count.resize(std::max(c.evd_count.n, c.energies.size()));
-  c.evd_count.zero(s);
+  if (only != 1) c.evd_count.zero(s);
   // every stencil energy gets its own compacted-list / M range, so pass B can
   // run once for all energies of a kind after their pass A
   int64_t evd_total = 0;
@@ -721,6 +724,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian) {
   for (size_t id = 0; id < c.energies.size(); ++id) {
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
+    if ((only == 0 && e.dynamic) || (only == 1 && !e.dynamic)) continue;
     Structure& st = c.S[e.dynamic ? 1 : 0];
     EnergyDev E = energy_dev(c, e);
     const int proj = project ? 1 : 0, wh = with_hessian ? 1 : 0;
@@ -788,11 +792,15 @@ void ctx_gather_all(Context& c) {
   }
 }
 
-void ctx_assemble(Context& c, bool project, bool with_hessian) {
+// only / join: the static energies were already launched on the second
+// stream (ys_minimize_step); evaluate the dynamic ones here, then wait for
+// the join event before the gather.
+void ctx_assemble(Context& c, bool project, bool with_hessian, int only, cudaEvent_t join) {
   if (c.seen_epoch != c.epoch)
     fail(YS_ERR_VALIDATION, "dynamic structures are stale after resize_dynamic; call refresh_dynamic()");
   record(c, 1);
-  ctx_eval_all(c, project, with_hessian);
+  ctx_eval_all(c, project, with_hessian, only);
+  if (join) YS_CUDA(cudaStreamWaitEvent(c.stream, join, 0));
   record(c, 2);
   if (with_hessian) {
     ctx_gather_all(c);

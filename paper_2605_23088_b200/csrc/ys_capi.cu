@@ -54,7 +54,6 @@ void ctx_gather_all(Context& c);
 bool spmv_variant(Context& c, int v, const double* x, double* y);
 void barrier_probe(Context& c, int n, int with_reduce);
 
-void ctx_eval_all(Context& c, bool project, bool with_hessian);
 
 namespace {
 
@@ -337,6 +336,12 @@ void ys_destroy(ys_context* c) {
     if (sub->pinned) cudaFreeHost(sub->pinned);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->stream2) {
+    cudaStreamSynchronize(c->stream2);
+    cudaStreamDestroy(c->stream2);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+  }
   c->subs.clear();
   cudaStream_t s = c->stream;
   delete c;
@@ -774,8 +779,34 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     auto t0 = std::chrono::steady_clock::now();
     c->launches = 0;
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
-    ctx_refresh_dynamic(*c, false);
-    ctx_assemble(*c, true, true);
+    // The static energies' evaluation (SNH, inertia: nearly all of the local
+    // work) does not depend on the dynamic structure: it runs on a second
+    // stream while the dynamic group is rebuilt (whose host synchronisations
+    // would otherwise leave the device idle).  YS_OVERLAP=0: sequential.
+    static const bool overlap = !(getenv("YS_OVERLAP") && std::string(getenv("YS_OVERLAP")) == "0");
+    bool dyn_stencil = false;
+    for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
+    if (overlap && !dyn_stencil) {
+      if (!c->stream2) {
+        YS_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        YS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        YS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+      }
+      YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+      YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+      ctx_eval_all(*c, true, true, 0, c->stream2);
+      YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
+      try {
+        ctx_refresh_dynamic(*c, false);
+        ctx_assemble(*c, true, true, 1, c->ev_join);
+      } catch (...) {
+        cudaStreamSynchronize(c->stream2);
+        throw;
+      }
+    } else {
+      ctx_refresh_dynamic(*c, false);
+      ctx_assemble(*c, true, true);
+    }
     const double t_asm = elapsed(t0);
     ctx_build_preconditioner(*c);
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));

@@ -246,6 +246,9 @@ struct Context {
   double pcg_phase_ms[4] = {0};
   int64_t launches = 0;
   cudaEvent_t ev[10] = {};
+  // second stream: the static energies' evaluation overlaps the dynamic rebuild
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   DistState dist;
   ContactScratch contact;
@@ -264,7 +267,8 @@ struct Context {
 void ctx_finalize(Context& c);
 void ctx_refresh_dynamic(Context& c, bool force);
 void ctx_build_group(Context& c, int which);
-void ctx_assemble(Context& c, bool project, bool with_hessian);
+void ctx_assemble(Context& c, bool project, bool with_hessian, int only = -1, cudaEvent_t join = nullptr);
+void ctx_eval_all(Context& c, bool project, bool with_hessian, int only = -1, cudaStream_t s = nullptr);
 double ctx_total_energy(Context& c, double* per_energy);
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y);
 void ctx_build_preconditioner(Context& c);
