@@ -18,6 +18,7 @@
 //      DiagAccumulator block (static H block + dynamic contributions one by
 //      one) and inverts it for the preconditioner.
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -776,9 +777,10 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
   flush();
 }
 
-void ctx_gather_all(Context& c) {
-  cudaStream_t s = c.stream;
+void ctx_gather_all(Context& c, int only, cudaStream_t s) {
+  if (!s) s = c.stream;
   for (int w = 0; w < 2; ++w) {
+    if (only >= 0 && w != only) continue;
     Structure& st = c.S[w];
     for (auto& g : st.groups) {
       const int rc = int(g[0] * g[1]);
@@ -795,23 +797,24 @@ void ctx_gather_all(Context& c) {
 // only / join: the static energies were already launched on the second
 // stream (ys_minimize_step); evaluate the dynamic ones here, then wait for
 // the join event before the gather.
-void ctx_assemble(Context& c, bool project, bool with_hessian, int only, cudaEvent_t join) {
+void ctx_assemble(Context& c, bool project, bool with_hessian, int only, cudaEvent_t join, bool check) {
   if (c.seen_epoch != c.epoch)
     fail(YS_ERR_VALIDATION, "dynamic structures are stale after resize_dynamic; call refresh_dynamic()");
   record(c, 1);
   ctx_eval_all(c, project, with_hessian, only);
-  if (join) YS_CUDA(cudaStreamWaitEvent(c.stream, join, 0));
   record(c, 2);
   if (with_hessian) {
-    ctx_gather_all(c);
-  } else {  // Engine::assemble zeroes both stores and the diagonal (engine.cpp:50-53)
+    ctx_gather_all(c, only);  // (only == 1: the static group was gathered on the second stream)
+    if (join) YS_CUDA(cudaStreamWaitEvent(c.stream, join, 0));
+  } else {
+    if (join) YS_CUDA(cudaStreamWaitEvent(c.stream, join, 0));  // Engine::assemble zeroes both stores and the diagonal (engine.cpp:50-53)
     for (int w = 0; w < 2; ++w) c.S[w].values.zero(c.stream);
     c.diag.zero(c.stream);
   }
   record(c, 3);
   ctx_block_rows(c, with_hessian);
   record(c, 4);
-  check_err(c);
+  if (check) check_err(c);
   c.assembled = true;
   c.assembled_h = with_hessian;
 }
@@ -847,22 +850,63 @@ void ctx_block_rows(Context& c, bool want_h) {
 }
 
 // Flags of the last preconditioner build -> regularized count / singular error.
-void ctx_build_preconditioner(Context& c) {
-  std::vector<int32_t> fl = c.bflag.to_host(c.stream);
-  std::vector<int32_t> st, rc;
-  int32_t reg = 0;
-  for (int64_t b = 0; b < c.NB; ++b) {
-    if (fl[b] == 1 || fl[b] == 2) ++reg;
-    if (fl[b] == 3 || fl[b] == 4) {
-      if (st.empty()) {
-        st = c.bstart.to_host(c.stream);
-        rc = c.brc.to_host(c.stream);
-      }
-      fail(YS_ERR_NUMERICAL, "diagonal block at DoF range [" + std::to_string(st[b]) + ", " +
-                                 std::to_string(st[b] + rc[b]) + ") is singular");
-    }
+// Preconditioner flags summarised on the device (regularised count, first
+// singular block) and read back together with the evaluation error flag: one
+// 12-byte copy and one synchronisation instead of downloading NB flags.
+__global__ void k_flag_summary(const int32_t* __restrict__ fl, int64_t nb, int* out) {
+  int reg = 0, first = INT_MAX;
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb; b += int64_t(gridDim.x) * blockDim.x) {
+    const int f = fl[b];
+    reg += (f == 1 || f == 2);
+    if ((f == 3 || f == 4) && b < first) first = int(b);
   }
-  c.regularized = reg;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    reg += __shfl_xor_sync(0xffffffffu, reg, off);
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (reg) atomicAdd(out, reg);
+    if (first != INT_MAX) atomicMin(out + 1, first);
+  }
+}
+
+static void* pinned_buf(Context& c) {
+  if (!c.pinned) YS_CUDA(cudaMallocHost(&c.pinned, 65536));
+  return c.pinned;
+}
+
+__global__ void k_flag_init(int* out) {
+  out[0] = 0;
+  out[1] = INT_MAX;
+}
+
+void ctx_build_preconditioner(Context& c) {
+  cudaStream_t s = c.stream;
+  c.flagsum.resize(4);
+  k_flag_init<<<1, 1, 0, s>>>(c.flagsum.p + 1);
+  k_flag_summary<<<int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.NB, kTB), 4 * sm_count()))), kTB, 0, s>>>(
+      c.bflag.p, c.NB, c.flagsum.p + 1);
+  YS_LAUNCH_CHECK();
+  YS_CUDA(cudaMemcpyAsync(c.flagsum.p, c.errflag.p, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  int* h = reinterpret_cast<int*>(pinned_buf(c));
+  YS_CUDA(cudaMemcpyAsync(h, c.flagsum.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  YS_CUDA(cudaStreamSynchronize(s));
+  if (h[0]) {  // evaluation error of the assembly (check_err, deferred to here by ys_minimize_step)
+    c.errflag.zero(s);
+    if (h[0] & kErrLog) fail(YS_ERR_NUMERICAL, "log of non-positive value");
+    fail(YS_ERR_NUMERICAL, "division by zero");
+  }
+  if (h[2] != INT_MAX) {
+    const int64_t b = h[2];
+    int32_t st = 0, rc = 0;
+    YS_CUDA(cudaMemcpyAsync(&st, c.bstart.p + b, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaMemcpyAsync(&rc, c.brc.p + b, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+    fail(YS_ERR_NUMERICAL, "diagonal block at DoF range [" + std::to_string(st) + ", " + std::to_string(st + rc) +
+                               ") is singular");
+  }
+  c.regularized = h[1];
 }
 
 double ctx_total_energy(Context& c, double* per_energy) {

@@ -50,7 +50,6 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
                  PcgState* st, double* part, int grid);
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
-void ctx_gather_all(Context& c);
 bool spmv_variant(Context& c, int v, const double* x, double* y);
 void barrier_probe(Context& c, int n, int with_reduce);
 
@@ -795,17 +794,18 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
       YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
       YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
       ctx_eval_all(*c, true, true, 0, c->stream2);
+      ctx_gather_all(*c, 0, c->stream2);
       YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
       try {
         ctx_refresh_dynamic(*c, false);
-        ctx_assemble(*c, true, true, 1, c->ev_join);
+        ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
       } catch (...) {
         cudaStreamSynchronize(c->stream2);
         throw;
       }
     } else {
       ctx_refresh_dynamic(*c, false);
-      ctx_assemble(*c, true, true);
+      ctx_assemble(*c, true, true, -1, nullptr, false);
     }
     const double t_asm = elapsed(t0);
     ctx_build_preconditioner(*c);

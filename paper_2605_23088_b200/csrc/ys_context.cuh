@@ -210,6 +210,7 @@ struct Context {
   std::vector<uint64_t> pcg_key;
   DevBuf<double> scratch;
   DevBuf<int> errflag;
+  DevBuf<int> flagsum;  // [eval error flag, regularised blocks, first singular block]
   // sliced-ELL full copy of H_static + H_dynamic for the uniform 3x3 PCG (ys_sell.cuh)
   DevBuf<int32_t> sell_len, sell_col;
   DevBuf<int32_t> sell_perm, sell_lenq;  // position -> row (rows sorted by length per window), length by position
@@ -267,8 +268,10 @@ struct Context {
 void ctx_finalize(Context& c);
 void ctx_refresh_dynamic(Context& c, bool force);
 void ctx_build_group(Context& c, int which);
-void ctx_assemble(Context& c, bool project, bool with_hessian, int only = -1, cudaEvent_t join = nullptr);
+void ctx_assemble(Context& c, bool project, bool with_hessian, int only = -1, cudaEvent_t join = nullptr,
+                  bool check = true);
 void ctx_eval_all(Context& c, bool project, bool with_hessian, int only = -1, cudaStream_t s = nullptr);
+void ctx_gather_all(Context& c, int only = -1, cudaStream_t s = nullptr);
 double ctx_total_energy(Context& c, double* per_energy);
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y);
 void ctx_build_preconditioner(Context& c);
