@@ -947,6 +947,165 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
 }
 
 // ---------------------------------------------------------------------------
+// Persistent PCG for mixed block sizes (affine bodies: 9 + 3 DoF rows next to
+// 3-DoF vertices; C3): the graph-looped kernels cost ~47 us per iteration in
+// launch latency on small systems.  Same phases and fixed-order reductions as
+// k_pcg33_stream; phase A is a warp per block row of each block-size class
+// (acc_gen), phases B / C one thread per block row / DoF.
+struct GenClasses {
+  int n;
+  int rc[8];
+  const int32_t* rows[8];  // null: all block rows (single class)
+  int64_t nrows[8];
+};
+
+template <int RC>
+__device__ __forceinline__ double gen_row(const SpmvDev& S0, const SpmvDev& S1, int has1, const BlocksDev& B,
+                                          int64_t R, int lane, const double* __restrict__ p, double* __restrict__ hp) {
+  double acc[RC];
+#pragma unroll
+  for (int i = 0; i < RC; ++i) acc[i] = 0.0;
+  acc_gen<RC>(S0, R, lane, p, acc);
+  if (has1) acc_gen<RC>(S1, R, lane, p, acc);
+#pragma unroll
+  for (int i = 0; i < RC; ++i)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
+  double dot = 0.0;
+  if (lane == 0) {
+    const int64_t s0 = B.start[R];
+#pragma unroll
+    for (int i = 0; i < RC; ++i) {
+      hp[s0 + i] = acc[i];
+      dot += p[s0 + i] * acc[i];
+    }
+  }
+  return dot;
+}
+
+__global__ void __launch_bounds__(kTB) k_pcg_gen_persistent(SpmvDev S0, SpmvDev S1, int has1, BlocksDev B,
+                                                            GenClasses cls, int64_t s, const double* __restrict__ minv,
+                                                            double* __restrict__ x, double* __restrict__ r,
+                                                            double* __restrict__ z, double* __restrict__ p,
+                                                            double* __restrict__ hp, PcgState* st, double* part,
+                                                            double* hist, GridBar* gb) {
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(G) * blockDim.x) >> 5;
+  const int64_t t0i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = int64_t(G) * blockDim.x;
+  const double gnorm = st->gnorm;
+  const double tol = st->tol;
+  const long long max_iter = st->max_iter;
+  const long long hist_cap = st->hist_cap;
+  double rz = st->rz;
+  int status = st->status;
+  long long it = 0;
+  double rel = st->rel, php = 0.0, alpha = 0.0;
+  unsigned long long epoch = 0;
+  unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long t0 = gtimer();
+  while (status == 0) {
+    // ---- phase A: hp = H p per block-size class, pHp partials
+    double dot[1] = {0.0};
+    for (int k = 0; k < cls.n; ++k) {
+      const int rc = cls.rc[k];
+      for (int64_t q = w0; q < cls.nrows[k]; q += nw) {
+        const int64_t R = cls.rows[k] ? cls.rows[k][q] : q;
+        switch (rc) {
+          case 1: dot[0] += gen_row<1>(S0, S1, has1, B, R, lane, p, hp); break;
+          case 2: dot[0] += gen_row<2>(S0, S1, has1, B, R, lane, p, hp); break;
+          case 3: dot[0] += gen_row<3>(S0, S1, has1, B, R, lane, p, hp); break;
+          case 4: dot[0] += gen_row<4>(S0, S1, has1, B, R, lane, p, hp); break;
+          case 6: dot[0] += gen_row<6>(S0, S1, has1, B, R, lane, p, hp); break;
+          case 9: dot[0] += gen_row<9>(S0, S1, has1, B, R, lane, p, hp); break;
+          default: dot[0] += gen_row<12>(S0, S1, has1, B, R, lane, p, hp); break;
+        }
+      }
+    }
+    block_reduce<1>(dot);
+    if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    unsigned long long t1 = gtimer();
+    ph[0] += t1 - t0;
+    t0 = t1;
+    double tot1[1];
+    reduce_partials_all<1>(part, G, tot1);
+    php = tot1[0];
+    if (!isfinite(php) || php <= 0.0) {
+      status = php == 0.0 ? 2 : 3;
+      break;
+    }
+    alpha = rz / php;
+    // ---- phase B: x += a p, r -= a hp, z = M^-1 r per block row, partials of r.r and r.z
+    double v[2] = {0.0, 0.0};
+    for (int64_t b = t0i; b < B.nb; b += nth) {
+      const int rc = B.rc[b];
+      const int64_t s0 = B.start[b];
+      double rr[16], zz[16];
+      for (int i = 0; i < rc; ++i) {
+        x[s0 + i] += alpha * p[s0 + i];
+        rr[i] = r[s0 + i] - alpha * __ldcg(hp + s0 + i);
+        r[s0 + i] = rr[i];
+      }
+      precond_apply_any(rc, minv + B.voff[b], rr, zz);
+      for (int i = 0; i < rc; ++i) {
+        z[s0 + i] = zz[i];
+        v[0] += rr[i] * rr[i];
+        v[1] += rr[i] * zz[i];
+      }
+    }
+    block_reduce<2>(v);
+    if (threadIdx.x == 0) {
+      part[G + blockIdx.x] = v[0];
+      part[2 * G + blockIdx.x] = v[1];
+    }
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    t1 = gtimer();
+    ph[1] += t1 - t0;
+    t0 = t1;
+    double tot2[2];
+    reduce_partials_all<2>(part + G, G, tot2);
+    t1 = gtimer();
+    ph[2] += t1 - t0;
+    t0 = t1;
+    rel = sqrt(tot2[0]) / gnorm;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && it + 1 < hist_cap) hist[it + 1] = rel;
+    ++it;
+    if (!isfinite(rel)) {
+      status = 4;
+      break;
+    }
+    if (rel <= tol) {
+      status = 1;
+      break;
+    }
+    if (it >= max_iter) {
+      status = 5;
+      break;
+    }
+    const double beta = tot2[1] / rz;
+    rz = tot2[1];
+    // ---- phase C: p = z + beta p
+    for (int64_t i = t0i; i < s; i += nth) p[i] = __ldcg(z + i) + beta * p[i];
+    grid_sync_counter(&gb->arrivals, (unsigned long long)G * ++epoch);
+    t1 = gtimer();
+    ph[3] += t1 - t0;
+    t0 = t1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->it += it;
+    st->rel = rel;
+    st->rz = rz;
+    st->php = php;
+    st->alpha = alpha;
+    st->status = status;
+    if (status == 3 || status == 4) st->fail_it = int(it - (status == 4 ? 1 : 0));
+    for (int k = 0; k < 4; ++k) st->phase_ns[k] = ph[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 
 void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, double* y, bool accumulate,
@@ -1219,6 +1378,66 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         void* args[] = {&d0, &d1, &sl, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
         YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
       }
+      PcgState fin{};
+      YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      YS_CUDA(cudaStreamSynchronize(s));
+      c.launches += 2;
+      for (int k = 0; k < 4; ++k) c.pcg_phase_ms[k] = double(fin.phase_ns[k]) * 1e-6;
+      c.hist_count = fin.status == 1 && fin.it == 0 && fin.gnorm == 0.0 ? 0 : fin.it + 1;
+      if (fin.status == 3)
+        fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
+                                   " (non-finite or negative curvature)");
+      if (fin.status == 4)
+        fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
+                                   " (non-finite residual)");
+      if (stats) {
+        stats->pcg_iterations = fin.it;
+        stats->pcg_converged = fin.status == 1 ? 1 : 0;
+        stats->pcg_residual = (fin.gnorm == 0.0) ? 0.0 : fin.rel;
+      }
+      return;
+    }
+  }
+  // Mixed block sizes: one persistent cooperative kernel (YS_PCG_GEN=graph keeps
+  // the graph-looped kernels).
+  static const bool gen_graph = getenv("YS_PCG_GEN") && std::string(getenv("YS_PCG_GEN")) == "graph";
+  if (!gen_graph && c.rc_classes.size() <= 8) {
+    GenClasses cls{};
+    cls.n = int(c.rc_classes.size());
+    for (int k = 0; k < cls.n; ++k) {
+      cls.rc[k] = c.rc_classes[size_t(k)];
+      cls.rows[k] = c.rc_classes.size() == 1 ? nullptr : c.rc_lists[size_t(k)].p;
+      cls.nrows[k] = c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[size_t(k)].n);
+    }
+    bool ok = true;
+    for (int k = 0; k < cls.n; ++k) {
+      const int rc = cls.rc[k];
+      ok = ok && (rc == 1 || rc == 2 || rc == 3 || rc == 4 || rc == 6 || rc == 9 || rc == 12);
+    }
+    if (ok) {
+      void* kern = reinterpret_cast<void*>(k_pcg_gen_persistent);
+      int occ = 0;
+      YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
+      occ = std::max(occ, 1);
+      // small systems: fewer CTAs (cheaper barriers); at least one warp per 4 block rows
+      const int64_t want = std::max<int64_t>(1, ceil_div(c.NB * 8, kTB));
+      int gsz = int(std::min<int64_t>(int64_t(occ) * sm_count(), std::max<int64_t>(want, sm_count())));
+      c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
+      c.gridbar.resize(sizeof(GridBar));
+      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
+      const bool has1 = c.S[1].n_blocks > 0;
+      SpmvDev d0 = spmv_dev(c.S[0]);
+      SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+      int h1 = has1 ? 1 : 0;
+      BlocksDev B = blocks_view(c);
+      int64_t sdofs = c.s;
+      const double* minv = c.minv.p;
+      double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *part = c.partials.p,
+             *hist = c.hist.p;
+      PcgState* stp = c.pcg.p;
+      GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
+      void* args[] = {&d0, &d1, &h1, &B, &cls, &sdofs, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
+      YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
       PcgState fin{};
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
