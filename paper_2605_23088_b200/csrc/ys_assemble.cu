@@ -215,10 +215,9 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_batch(const __grid_const
   }
 }
 
-__global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* __restrict__ X, int project,
-                                                    int want_h, double* __restrict__ hc, double* __restrict__ gc) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= E.n) return;
+__device__ __forceinline__ void ortho_instance(const EnergyDev& E, int64_t i, const double* __restrict__ X,
+                                               int project, int want_h, double* __restrict__ hc,
+                                               double* __restrict__ gc) {
   double A[9];
   const double* q = X + E.startP + 9 * i;
 #pragma unroll
@@ -228,6 +227,13 @@ __global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* _
   double* go = gc + inst_goff(E, i);
 #pragma unroll
   for (int k = 0; k < 9; ++k) go[k] = g[k];
+}
+
+__global__ void __launch_bounds__(128) k_eval_ortho(EnergyDev E, const double* __restrict__ X, int project,
+                                                    int want_h, double* __restrict__ hc, double* __restrict__ gc) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  ortho_instance(E, i, X, project, want_h, hc, gc);
 }
 
 // Inertia of free points: one 3x3 block m I (projection: max(m, 0) I).
@@ -311,10 +317,9 @@ __global__ void k_eval_pair_free(EnergyDev E, const double* __restrict__ X, int 
 
 // Inertia over affine points and pair energies over unions with affine
 // bodies: one 3-vector delta, linear in the compressed DoFs.
-__global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int project, int want_h,
-                             double* __restrict__ hc, double* __restrict__ gc, int* err) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= E.n) return;
+__device__ __forceinline__ void point_instance(const EnergyDev& E, int64_t i, const double* __restrict__ X,
+                                               int project, int want_h, double* __restrict__ hc,
+                                               double* __restrict__ gc, int* err) {
   PSlot s[kMaxKappa];
   energy_slots(E, i, s);
   double dl[3], gd[3], P[9];
@@ -353,6 +358,35 @@ __global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int proj
     make_ublocks(s, E.kappa, u);
     write_point_blocks(u, P, hc + inst_hoff(E, i));
   }
+}
+
+__global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int project, int want_h,
+                             double* __restrict__ hc, double* __restrict__ gc, int* err) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  point_instance(E, i, X, project, want_h, hc, gc, err);
+}
+
+// Many small energies of one kind (C3: 64 affine bodies, each with its own
+// orthogonality and inertia energy of one / 27 instances) in one launch:
+// thread t -> energy j (prefix[j] <= t < prefix[j + 1]), instance t - prefix[j].
+// Each instance is computed exactly as by the per-energy kernels.
+template <int KIND>  // 0: orthogonality, 1: point terms (k_eval_point)
+__global__ void __launch_bounds__(128) k_eval_multi(const EnergyDev* __restrict__ Es, const int64_t* __restrict__ prefix,
+                                                    int ne, const double* __restrict__ X, int project, int want_h,
+                                                    double* __restrict__ hc, double* __restrict__ gc, int* err) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= prefix[ne]) return;
+  int lo = 0, hi = ne - 1;  // last j with prefix[j] <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const EnergyDev& E = Es[lo];
+  const int64_t i = t - prefix[lo];
+  if (KIND == 0) ortho_instance(E, i, X, project, want_h, hc, gc);
+  else point_instance(E, i, X, project, want_h, hc, gc, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -722,6 +756,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
     pending.clear();
     pending_n = 0;
   };
+  std::vector<size_t> multi[2][2];  // [group][0: orthogonality, 1: point-term inertia]
   for (size_t id = 0; id < c.energies.size(); ++id) {
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
@@ -754,14 +789,15 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
         break;
       }
       case K_ORTHO:
-        k_eval_ortho<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
-        break;
+        multi[e.dynamic ? 1 : 0][0].push_back(id);  // launched batched below
+        continue;
       case K_INERTIA:
-        if (c.domains[e.domain].kind == YS_POINTS_FREE)
+        if (c.domains[e.domain].kind == YS_POINTS_FREE) {
           k_eval_inertia_free<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p);
-        else
-          k_eval_point<<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
-                                                          c.errflag.p);
+        } else {
+          multi[e.dynamic ? 1 : 0][1].push_back(id);
+          continue;
+        }
         break;
       default:
         if (E.uni.kappa_u == 1)
@@ -775,6 +811,54 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
     ++c.launches;
   }
   flush();
+  // many small energies of one kind and group: one launch (k_eval_multi)
+  {
+    const int proj = project ? 1 : 0, wh = with_hessian ? 1 : 0;
+    std::vector<EnergyDev> es;
+    std::vector<int64_t> pre;
+    struct Launch {
+      int kind, group;
+      size_t e0, ne, p0;
+    };
+    std::vector<Launch> ls;
+    for (int g = 0; g < 2; ++g)
+      for (int kind = 0; kind < 2; ++kind) {
+        if (multi[g][kind].empty()) continue;
+        Launch l{kind, g, es.size(), multi[g][kind].size(), pre.size()};
+        int64_t acc = 0;
+        for (size_t id : multi[g][kind]) {
+          es.push_back(energy_dev(c, c.energies[id]));
+          pre.push_back(acc);
+          acc += c.energies[id].n;
+        }
+        pre.push_back(acc);
+        ls.push_back(l);
+      }
+    if (!ls.empty()) {
+      const int slot = only == 1 ? 1 : 0;
+      DevBuf<unsigned char>& me = c.multi_e[slot];
+      DevBuf<int64_t>& mp = c.multi_pre[slot];
+      me.resize(es.size() * sizeof(EnergyDev));
+      mp.resize(pre.size());
+      YS_CUDA(cudaMemcpyAsync(me.p, es.data(), es.size() * sizeof(EnergyDev), cudaMemcpyHostToDevice, s));
+      YS_CUDA(cudaMemcpyAsync(mp.p, pre.data(), pre.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      const EnergyDev* de = reinterpret_cast<const EnergyDev*>(me.p);
+      for (const Launch& l : ls) {
+        Structure& st = c.S[l.group];
+        const int64_t total = pre[l.p0 + l.ne];
+        if (total == 0) continue;
+        const unsigned grid = grid_for(total, 128);
+        if (l.kind == 0)
+          k_eval_multi<0><<<grid, 128, 0, s>>>(de + l.e0, mp.p + l.p0, int(l.ne), c.X.p, proj, wh,
+                                               st.hcontrib.p, st.gcontrib.p, c.errflag.p);
+        else
+          k_eval_multi<1><<<grid, 128, 0, s>>>(de + l.e0, mp.p + l.p0, int(l.ne), c.X.p, proj, wh,
+                                               st.hcontrib.p, st.gcontrib.p, c.errflag.p);
+        YS_LAUNCH_CHECK();
+        ++c.launches;
+      }
+    }
+  }
 }
 
 void ctx_gather_all(Context& c, int only, cudaStream_t s) {

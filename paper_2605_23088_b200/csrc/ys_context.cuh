@@ -210,7 +210,11 @@ struct Context {
   std::vector<uint64_t> pcg_key;
   DevBuf<double> scratch;
   DevBuf<int> errflag;
-  DevBuf<int> flagsum;  // [eval error flag, regularised blocks, first singular block]
+  DevBuf<int> flagsum;
+  // EnergyDev arrays of batched small energies (k_eval_multi); [1] for the
+  // dynamic-only call, which may run concurrently with the static one
+  DevBuf<unsigned char> multi_e[2];
+  DevBuf<int64_t> multi_pre[2];  // [eval error flag, regularised blocks, first singular block]
   // sliced-ELL full copy of H_static + H_dynamic for the uniform 3x3 PCG (ys_sell.cuh)
   DevBuf<int32_t> sell_len, sell_col;
   DevBuf<int32_t> sell_perm, sell_lenq;  // position -> row (rows sorted by length per window), length by position
