@@ -670,6 +670,51 @@ __global__ void k_block_rows(BlocksDev B, const int32_t* __restrict__ list, int6
   block_row_work<N>(b, B, S0, S1, G, diag, minv, bflag, want_h);
 }
 
+// Large blocks (affine bodies' 9x9 A block, 12x12): a warp per block row.
+// Lane l accumulates entries l, l + 32, ... over the contributions in the same
+// order as block_row_work (per entry the same sums, bit for bit); the row's
+// whole diagonal block then goes through one lane's inverse.  (C3: 64 bodies
+// each collecting ~100 contact blocks serially took 260 us in one thread.)
+template <int N>
+__global__ void k_block_rows_warp(BlocksDev B, const int32_t* __restrict__ list, int64_t nb, GroupView S0,
+                                  GroupView S1, double* G, double* diag, double* minv, int32_t* bflag, int want_h) {
+  const int64_t q = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= nb) return;
+  const int64_t b = list ? list[q] : q;
+  const int32_t st = B.start[b];
+  for (int k = lane; k < N; k += 32) {
+    double acc = 0.0;
+    for (int gi = 0; gi < 2; ++gi) {
+      const GroupView& S = gi == 0 ? S0 : S1;
+      if (!S.gseg) continue;
+      const int32_t j0 = S.gseg[b], j1 = S.gseg[b + 1];
+      for (int32_t j = j0; j < j1; ++j) acc += S.gcontrib[(S.gperm[j] & 0x0FFFFFFFu) + k];
+    }
+    G[st + k] = acc;
+  }
+  if (!want_h) return;
+  double* dd = diag + B.voff[b];
+  const int32_t u0 = S0.diag_uid ? S0.diag_uid[b] : -1;
+  const int32_t u1 = S1.diag_uid ? S1.diag_uid[b] : -1;
+  for (int k = lane; k < N * N; k += 32) {
+    double v = 0.0;
+    if (u0 >= 0) v = 0.0 + S0.values[S0.voff[u0] + k];
+    if (u1 >= 0) {
+      const int64_t j0 = S1.seg[u1], j1 = S1.seg[u1 + 1];
+      for (int64_t j = j0; j < j1; ++j) v += S1.hcontrib[S1.perm[j] + k];
+    }
+    dd[k] = v;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double blk[N * N];
+#pragma unroll
+    for (int k = 0; k < N * N; ++k) blk[k] = dd[k];
+    bflag[b] = jacobi_block_inverse<N>(blk, minv + B.voff[b]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Host orchestration
 
@@ -912,6 +957,16 @@ void ctx_block_rows(Context& c, bool want_h) {
     const int64_t nb = c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[k].n);
     if (nb == 0) continue;
     const unsigned g = grid_for(nb, 128);
+    if (c.rc_classes[k] == 9 || c.rc_classes[k] == 12) {
+      const unsigned gw = grid_for(nb * 32, 128);
+      if (c.rc_classes[k] == 9)
+        k_block_rows_warp<9><<<gw, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh);
+      else
+        k_block_rows_warp<12><<<gw, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh);
+      YS_LAUNCH_CHECK();
+      ++c.launches;
+      continue;
+    }
 #define YS_ROWS(N)                                                                                            \
   case N:                                                                                                     \
     k_block_rows<N><<<g, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); \
