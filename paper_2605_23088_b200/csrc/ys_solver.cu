@@ -983,6 +983,35 @@ __device__ __forceinline__ double gen_row(const SpmvDev& S0, const SpmvDev& S1, 
   return dot;
 }
 
+template <int N>
+__device__ __forceinline__ void gen_update(const BlocksDev& B, int64_t b, double alpha, const double* __restrict__ minv,
+                                           double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                                           const double* __restrict__ p, const double* __restrict__ hp,
+                                           double (&v)[2]) {
+  const int64_t s0 = B.start[b];
+  double rr[N], zz[N], pp[N], xx[N], hh[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    pp[i] = p[s0 + i];
+    xx[i] = x[s0 + i];
+    rr[i] = r[s0 + i];
+    hh[i] = __ldcg(hp + s0 + i);
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    x[s0 + i] = xx[i] + alpha * pp[i];
+    rr[i] = rr[i] - alpha * hh[i];
+    r[s0 + i] = rr[i];
+  }
+  precond_apply<N>(minv + B.voff[b], rr, zz);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    z[s0 + i] = zz[i];
+    v[0] += rr[i] * rr[i];
+    v[1] += rr[i] * zz[i];
+  }
+}
+
 __global__ void __launch_bounds__(kTB) k_pcg_gen_persistent(SpmvDev S0, SpmvDev S1, int has1, BlocksDev B,
                                                             GenClasses cls, int64_t s, const double* __restrict__ minv,
                                                             double* __restrict__ x, double* __restrict__ r,
@@ -1041,18 +1070,25 @@ __global__ void __launch_bounds__(kTB) k_pcg_gen_persistent(SpmvDev S0, SpmvDev 
     double v[2] = {0.0, 0.0};
     for (int64_t b = t0i; b < B.nb; b += nth) {
       const int rc = B.rc[b];
-      const int64_t s0 = B.start[b];
-      double rr[16], zz[16];
-      for (int i = 0; i < rc; ++i) {
-        x[s0 + i] += alpha * p[s0 + i];
-        rr[i] = r[s0 + i] - alpha * __ldcg(hp + s0 + i);
-        r[s0 + i] = rr[i];
-      }
-      precond_apply_any(rc, minv + B.voff[b], rr, zz);
-      for (int i = 0; i < rc; ++i) {
-        z[s0 + i] = zz[i];
-        v[0] += rr[i] * rr[i];
-        v[1] += rr[i] * zz[i];
+      switch (rc) {  // unrolled (independent loads) for the common sizes
+        case 3: gen_update<3>(B, b, alpha, minv, x, r, z, p, hp, v); break;
+        case 9: gen_update<9>(B, b, alpha, minv, x, r, z, p, hp, v); break;
+        case 12: gen_update<12>(B, b, alpha, minv, x, r, z, p, hp, v); break;
+        default: {
+          const int64_t s0 = B.start[b];
+          double rr[16], zz[16];
+          for (int i = 0; i < rc; ++i) {
+            x[s0 + i] += alpha * p[s0 + i];
+            rr[i] = r[s0 + i] - alpha * __ldcg(hp + s0 + i);
+            r[s0 + i] = rr[i];
+          }
+          precond_apply_any(rc, minv + B.voff[b], rr, zz);
+          for (int i = 0; i < rc; ++i) {
+            z[s0 + i] = zz[i];
+            v[0] += rr[i] * rr[i];
+            v[1] += rr[i] * zz[i];
+          }
+        }
       }
     }
     block_reduce<2>(v);
