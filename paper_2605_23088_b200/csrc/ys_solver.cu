@@ -217,6 +217,20 @@ bool spmv_variant(Context& c, int v, const double* x, double* y) {
 
 // Generic shapes: one warp per block row of size RC (launched per block-size
 // class), lanes over the row's entries, fixed xor-butterfly reduction.
+// One block of row R's list: y_R += B^T x_other (TR, B is OT x RC) or
+// B x_other (B is RC x OT), OT the other side's block size (compile time).
+template <int RC, int OT, bool TR>
+__device__ __forceinline__ void acc_block(const double* __restrict__ v, const double* __restrict__ xo,
+                                          double (&acc)[RC]) {
+  double xk[OT];
+#pragma unroll
+  for (int k = 0; k < OT; ++k) xk[k] = xo[k];
+#pragma unroll
+  for (int k = 0; k < OT; ++k)
+#pragma unroll
+    for (int i = 0; i < RC; ++i) acc[i] += (TR ? v[k * RC + i] : v[i * OT + k]) * xk[k];
+}
+
 template <int RC>
 __device__ __forceinline__ void acc_gen(const SpmvDev& S, int64_t R, int lane, const double* __restrict__ x,
                                         double (&acc)[RC]) {
@@ -227,13 +241,21 @@ __device__ __forceinline__ void acc_gen(const SpmvDev& S, int64_t R, int lane, c
     const int r = S.br[u], c = S.bc[u];
     const double* v = S.values + S.voff[u];
     const double* xo = x + S.oth[j];
-    if (e >> 31) {  // block (other, R): y_R += B^T x_other, B is r x RC
+    const bool tr = (e >> 31) != 0;  // block (other, R): B is r x RC; else block (R, other): B is RC x c
+    const int ot = tr ? r : c;
+    if (ot == 3) {  // the common shapes unrolled (loads issued together)
+      if (tr) acc_block<RC, 3, true>(v, xo, acc);
+      else acc_block<RC, 3, false>(v, xo, acc);
+    } else if (ot == 9) {
+      if (tr) acc_block<RC, 9, true>(v, xo, acc);
+      else acc_block<RC, 9, false>(v, xo, acc);
+    } else if (tr) {
       for (int k = 0; k < r; ++k) {
         const double xk = xo[k];
 #pragma unroll
         for (int i = 0; i < RC; ++i) acc[i] += v[k * RC + i] * xk;
       }
-    } else {  // block (R, other): y_R += B x_other, B is RC x c
+    } else {
       for (int k = 0; k < c; ++k) {
         const double xk = xo[k];
 #pragma unroll
