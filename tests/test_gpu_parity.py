@@ -320,3 +320,31 @@ def test_contact_candidates_grid_bit_exact(dhat):
     assert np.array_equal(g.get_pairs(pg), o.get_pairs(po))
     if dhat >= 0.01:
         assert ng > 0
+
+
+def test_overlap_and_sequential_steps_are_bitwise_equal():
+    """The static energies' evaluation on the second stream (overlapping the
+    dynamic rebuild) must give exactly the sequential step (YS_OVERLAP=0)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import hashlib, numpy as np\n"
+        "from paper_2605_23088_b200 import configs\n"
+        "from paper_2605_23088_b200.scene import SimConfig, Simulation\n"
+        "cfg = SimConfig.from_dict(configs.c3())\n"
+        "sim = Simulation(cfg, backend='gpu')\n"
+        "configs.jitter_targets(sim, 0.002)\n"
+        "sim.begin_frame(); sim.refresh_dynamic_pairs()\n"
+        "st = sim.eng.minimize_step(1e-4)\n"
+        "print(hashlib.sha256(np.ascontiguousarray(st.dx).tobytes()).hexdigest(), st.pcg_iterations)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for ov in ("1", "0"):
+        env = dict(os.environ, YS_OVERLAP=ov, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
