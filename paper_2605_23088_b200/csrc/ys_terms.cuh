@@ -50,9 +50,9 @@ YS_HD constexpr double kST(int a, int i) { return a == 0 ? -1.0 : (i == a - 1 ? 
 
 // ---------------------------------------------------------------------------
 // Cyclic Jacobi on a packed symmetric 9x9 matrix, eigenvectors in v (row-major
-// v[k*9+j] = component k of eigenvector j).  Per rotation one sqrt, one
-// division and one rsqrt: with h = a_qq - a_pp,
-//   t = 2 sgn(h) a_pq / (|h| + sqrt(h^2 + 4 a_pq^2)),  c = 1/sqrt(1 + t^2),  s = t c
+// v[k*9+j] = component k of eigenvector j).  Per rotation two rsqrt and no
+// division: with h = a_qq - a_pp the rotation of
+//   t = 2 sgn(h) a_pq / (|h| + sqrt(h^2 + 4 a_pq^2))
 // (the smaller root of t^2 + 2 theta t - 1 = 0, theta = h / (2 a_pq)).
 // Rotations whose off-diagonal entry is below the rounding of both diagonal
 // entries are dropped (the classical negligibility rule); when every lane of
@@ -72,14 +72,21 @@ __device__ __forceinline__ void jacobi_rot(double* a, double* v, int p, int q) {
     a[pk9(p, q)] = 0.0;
     return;
   }
-  double t = 0.0;
+  // tan(theta) = 2 sgn(h) a_pq / (|h| + sqrt(h^2 + 4 a_pq^2)) through two
+  // reciprocal square roots and no division / square root:
+  //   rd = 1 / sqrt(h^2 + 4 a_pq^2), c^2 = (1 + |h| rd) / 2, rc = 1 / c,
+  //   s = sgn(h) a_pq rd rc, t = s rc   (c^2 + s^2 = 1 up to rounding)
+  double t = 0.0, c = 1.0, sn = 0.0;
   if (!negligible) {
     const double h = aqq - app;
-    const double num = h < 0.0 ? -2.0 * apq : 2.0 * apq;
-    t = num / (fabs(h) + sqrt(h * h + 4.0 * apq * apq));
+    const double sa = h < 0.0 ? -apq : apq;
+    const double rd = rsqrt(h * h + 4.0 * apq * apq);
+    const double c2 = 0.5 + 0.5 * (fabs(h) * rd);
+    const double rc = rsqrt(c2);
+    c = c2 * rc;
+    sn = sa * rd * rc;
+    t = sn * rc;
   }
-  const double c = rsqrt(1.0 + t * t);
-  const double sn = t * c;
   const double tq = t * apq;
   a[pk9(p, p)] = app - tq;
   a[pk9(q, q)] = aqq + tq;
