@@ -1397,7 +1397,10 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         void* kern = (void*)k_pcg33_stream<SellPhaseA>;
         const int wpb = kTB / 32;
         for (int per = kSpmvMinB; per >= 1 && !launched; --per) {
-          int gsz = per * sm_count();
+          // small systems: no more CTAs than give every warp two slices (at
+          // least one per SM) — the grid barriers get cheaper with fewer CTAs
+          int gsz = int(std::min<int64_t>(int64_t(per) * sm_count(),
+                                          std::max<int64_t>(sm_count(), ceil_div(c.sell_slices, int64_t(wpb) * 2))));
           int K = int(ceil_div(c.sell_slices, int64_t(gsz) * wpb));
           int TW = sell_max_warp_rows(c, int64_t(gsz) * wpb, K);
           const size_t smem = size_t(wpb) * K * 8 + size_t(wpb) * K * 32 * 4 + size_t(wpb) * TW * 32 * 4;
