@@ -486,12 +486,16 @@ int ys_set_pairs(ys_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
     if (n < 0) fail(YS_ERR_VALIDATION, "negative instance count");
     check_pairs_in_range(*c, p, n, pairs);
     p.n = n;
-    p.h_pairs.assign(pairs, pairs + 2 * n);
-    p.host_stale = false;
     if (c->finalized) {
+      // the device copy is authoritative; ys_get_pairs downloads it lazily.  The
+      // pageable upload has staged q before returning, so no synchronisation.
       std::vector<int32_t> q(pairs, pairs + 2 * n);
       p.pairs.upload(q, c->stream);
-      YS_CUDA(cudaStreamSynchronize(c->stream));
+      p.h_pairs.clear();
+      p.host_stale = n > 0;
+    } else {
+      p.h_pairs.assign(pairs, pairs + 2 * n);
+      p.host_stale = false;
     }
     ++c->epoch;  // Scene::bump_dynamic_epoch (scene.cpp:198)
   });
