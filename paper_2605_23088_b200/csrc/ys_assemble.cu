@@ -753,10 +753,12 @@ static void record(Context& c, int idx) {
 // only: -1 every energy, 0 the static group's, 1 the dynamic group's; s: the
 // stream to launch on (default: the context stream).  The pass-B counters are
 // zeroed by the call that evaluates the static group (the stencil energies).
-void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStream_t s) {
+// part: -1 every selected energy, 0 / 1 only those with an even / odd index
+// (two streams share the static energies; the caller zeroes the counters).
+void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStream_t s, int part, bool zero_counts) {
   if (!s) s = c.stream;
   c.evd_count.resize(std::max(c.evd_count.n, c.energies.size()));
-  if (only != 1) c.evd_count.zero(s);
+  if (only != 1 && zero_counts) c.evd_count.zero(s);
   // every stencil energy gets its own compacted-list / M range, so pass B can
   // run once for all energies of a kind after their pass A
   int64_t evd_total = 0;
@@ -806,6 +808,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
     Energy& e = c.energies[id];
     if (e.n == 0 || e.kappa == 0) continue;
     if ((only == 0 && e.dynamic) || (only == 1 && !e.dynamic)) continue;
+    if (part >= 0 && int(id % 2) != part) continue;
     Structure& st = c.S[e.dynamic ? 1 : 0];
     EnergyDev E = energy_dev(c, e);
     const int proj = project ? 1 : 0, wh = with_hessian ? 1 : 0;
@@ -880,7 +883,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
         ls.push_back(l);
       }
     if (!ls.empty()) {
-      const int slot = only == 1 ? 1 : 0;
+      const int slot = only == 1 ? 1 : part == 1 ? 2 : 0;
       DevBuf<unsigned char>& me = c.multi_e[slot];
       DevBuf<int64_t>& mp = c.multi_pre[slot];
       me.resize(es.size() * sizeof(EnergyDev));

@@ -337,9 +337,12 @@ void ys_destroy(ys_context* c) {
     if (e) cudaEventDestroy(e);
   if (c->stream2) {
     cudaStreamSynchronize(c->stream2);
+    cudaStreamSynchronize(c->stream3);
     cudaStreamDestroy(c->stream2);
+    cudaStreamDestroy(c->stream3);
     cudaEventDestroy(c->ev_fork);
     cudaEventDestroy(c->ev_join);
+    cudaEventDestroy(c->ev_join3);
   }
   c->subs.clear();
   cudaStream_t s = c->stream;
@@ -792,12 +795,22 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     if (overlap && !dyn_stencil) {
       if (!c->stream2) {
         YS_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        YS_CUDA(cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking));
         YS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         YS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        YS_CUDA(cudaEventCreateWithFlags(&c->ev_join3, cudaEventDisableTiming));
       }
+      // the static energies split over two streams (even / odd index): one
+      // energy's pass-B tail overlaps the other stream's work
+      c->evd_count.resize(std::max(c->evd_count.n, c->energies.size()));
+      c->evd_count.zero(c->stream);
       YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
       YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
-      ctx_eval_all(*c, true, true, 0, c->stream2);
+      YS_CUDA(cudaStreamWaitEvent(c->stream3, c->ev_fork, 0));
+      ctx_eval_all(*c, true, true, 0, c->stream2, 0, false);
+      ctx_eval_all(*c, true, true, 0, c->stream3, 1, false);
+      YS_CUDA(cudaEventRecord(c->ev_join3, c->stream3));
+      YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_join3, 0));
       ctx_gather_all(*c, 0, c->stream2);
       YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
       try {
@@ -805,6 +818,7 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
         ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
       } catch (...) {
         cudaStreamSynchronize(c->stream2);
+        cudaStreamSynchronize(c->stream3);
         throw;
       }
     } else {

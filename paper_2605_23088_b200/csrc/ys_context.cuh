@@ -211,10 +211,10 @@ struct Context {
   DevBuf<double> scratch;
   DevBuf<int> errflag;
   DevBuf<int> flagsum;
-  // EnergyDev arrays of batched small energies (k_eval_multi); [1] for the
-  // dynamic-only call, which may run concurrently with the static one
-  DevBuf<unsigned char> multi_e[2];
-  DevBuf<int64_t> multi_pre[2];  // [eval error flag, regularised blocks, first singular block]
+  // EnergyDev arrays of batched small energies (k_eval_multi); one per call
+  // that may run concurrently: [0] static / all, [1] dynamic, [2] odd static part
+  DevBuf<unsigned char> multi_e[3];
+  DevBuf<int64_t> multi_pre[3];  // [eval error flag, regularised blocks, first singular block]
   // sliced-ELL full copy of H_static + H_dynamic for the uniform 3x3 PCG (ys_sell.cuh)
   DevBuf<int32_t> sell_len, sell_col;
   DevBuf<int32_t> sell_perm, sell_lenq;  // position -> row (rows sorted by length per window), length by position
@@ -252,8 +252,8 @@ struct Context {
   int64_t launches = 0;
   cudaEvent_t ev[10] = {};
   // second stream: the static energies' evaluation overlaps the dynamic rebuild
-  cudaStream_t stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream2 = nullptr, stream3 = nullptr;  // stream3: the odd static energies
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join3 = nullptr;
 
   DistState dist;
   ContactScratch contact;
@@ -274,7 +274,8 @@ void ctx_refresh_dynamic(Context& c, bool force);
 void ctx_build_group(Context& c, int which);
 void ctx_assemble(Context& c, bool project, bool with_hessian, int only = -1, cudaEvent_t join = nullptr,
                   bool check = true);
-void ctx_eval_all(Context& c, bool project, bool with_hessian, int only = -1, cudaStream_t s = nullptr);
+void ctx_eval_all(Context& c, bool project, bool with_hessian, int only = -1, cudaStream_t s = nullptr,
+                  int part = -1, bool zero_counts = true);
 void ctx_gather_all(Context& c, int only = -1, cudaStream_t s = nullptr);
 double ctx_total_energy(Context& c, double* per_energy);
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y);
