@@ -784,6 +784,7 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     require_finalized(*c);
     auto t0 = std::chrono::steady_clock::now();
     c->launches = 0;
+    c->sell_prepared = false;
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
     // The static energies' evaluation (SNH, inertia: nearly all of the local
     // work) does not depend on the dynamic structure: it runs on a second
@@ -815,8 +816,12 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
       YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
       try {
         ctx_refresh_dynamic(*c, false);
+        // the solve's copy layout needs the structure only: built while the
+        // static evaluation still runs on the side streams
+        if (!c->dist.kind) pcg_prepare(*c);
         ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
       } catch (...) {
+        c->sell_prepared = false;
         cudaStreamSynchronize(c->stream2);
         cudaStreamSynchronize(c->stream3);
         throw;
@@ -826,7 +831,12 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
       ctx_assemble(*c, true, true, -1, nullptr, false);
     }
     const double t_asm = elapsed(t0);
-    ctx_build_preconditioner(*c);
+    try {
+      ctx_build_preconditioner(*c);
+    } catch (...) {
+      c->sell_prepared = false;  // the prepared layout is consumed by this step's solve only
+      throw;
+    }
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));
     if (max_iter < 0) max_iter = std::max<int64_t>(2 * c->s, 64);
     ys_step_stats local{};

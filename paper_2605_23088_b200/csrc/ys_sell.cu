@@ -207,12 +207,38 @@ SellDev sell_dev(Context& c) {
 // Builds the sliced-ELL copy of S[0] + S[1] (uniform 3x3 systems only) with H
 // lanes per block row, over the block rows [r0, r1) (r1 < 0: all rows).  One host synchronisation (the entry-row count sizes
 // the buffers).
+// The copy's layout (entry counts, window sort, slice widths, offsets) depends
+// on the block structure only; sell_prepare builds it ahead of the values —
+// Newton steps call it right after the dynamic rebuild, while the static
+// evaluation still runs on the side streams — and the next sell_build with the
+// same (H, r0, r1) only fills the values.
+static void sell_layout(Context& c, int H, int64_t r0, int64_t r1);
+
+void sell_prepare(Context& c, int H, int64_t r0, int64_t r1) {
+  if (r1 < 0) r1 = c.NB;
+  sell_layout(c, H, r0, r1);
+  c.sell_prepared = true;
+}
+
 void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
+  if (r1 < 0) r1 = c.NB;
+  const bool ready = c.sell_prepared && c.sell_h == H && c.sell_r0 == r0 && c.sell_r1 == r1;
+  c.sell_prepared = false;
+  if (!ready) sell_layout(c, H, r0, r1);
+  if (r1 - r0 == 0) return;
+  const bool has1 = c.S[1].n_blocks > 0;
+  SpmvDev d0 = spmv_dev(c.S[0]);
+  SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+  k_sell_fill_lanes<<<int(ceil_div(c.sell_slices * 32, kTB)), kTB, 0, c.stream>>>(
+      d0, d1, has1 ? 1 : 0, r0, r1, H, c.sell_perm.p, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
+  YS_LAUNCH_CHECK();
+}
+
+static void sell_layout(Context& c, int H, int64_t r0, int64_t r1) {
   cudaStream_t s = c.stream;
   const bool has1 = c.S[1].n_blocks > 0;
   SpmvDev d0 = spmv_dev(c.S[0]);
   SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
-  if (r1 < 0) r1 = c.NB;
   const int64_t nb = r1 - r0;
   const int rps = 32 / H;
   const int64_t nsl = ceil_div(nb, rps);
@@ -257,9 +283,6 @@ void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   c.sell_tw_host = tw;
   c.sell_col.resize(size_t(rows * 32 + 4));
   c.sell_val.resize(size_t(rows * 288 + 4));
-  k_sell_fill_lanes<<<int(ceil_div(nsl * 32, kTB)), kTB, 0, s>>>(
-      d0, d1, has1 ? 1 : 0, r0, r1, H, c.sell_perm.p, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, H, r0});
-  YS_LAUNCH_CHECK();
 }
 
 template <int H>

@@ -1344,6 +1344,17 @@ void drop_pcg_graph(Context& c) {
 
 int pcg_grid(Context& c) { return std::max(1, sm_count() * 8); }
 
+// The layout half of the uniform-3x3 solve's sliced-ELL build (sell_prepare),
+// when the next ctx_pcg will take that path.
+void pcg_prepare(Context& c) {
+  const bool has1 = c.S[1].n_blocks > 0;
+  const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
+  const char* pe = getenv("YS_PCG_PERSISTENT");
+  const char* se = getenv("YS_PCG_SELL");
+  if (!fast || (pe && std::string(pe) == "0") || (se && atoi(se) != 4)) return;
+  sell_prepare(c, 4);
+}
+
 void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev, ys_step_stats* stats) {
   cudaStream_t s = c.stream;
   const int grid = pcg_grid(c);
