@@ -135,6 +135,7 @@ _SIGS = {
     "bump_dynamic_epoch": [_P],
     "stream": [_P, C.POINTER(C.c_void_p)],
     "time_kernel": [_P, _I32, _I32, _PD, _PD],
+    "pcg_layout_info": [_P, _PI64, _PI64],
     "dist_unique_id": [C.c_char_p],
     "dist_init_nccl": [_P, _I32, _I32, C.c_char_p],
     "dist_init_host": [_P, _I32, _I32, ALLGATHER_FN, _P],
@@ -144,7 +145,7 @@ _SIGS = {
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
-OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream", "dist_unique_id",
+OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "pcg_layout_info", "stream", "dist_unique_id",
             "dist_init_nccl"}
 
 

@@ -785,6 +785,7 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     auto t0 = std::chrono::steady_clock::now();
     c->launches = 0;
     c->sell_prepared = false;
+    c->sym.prepared = false;
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
     // The static energies' evaluation (SNH, inertia: nearly all of the local
     // work) does not depend on the dynamic structure: it runs on a second
@@ -1005,7 +1006,7 @@ int ys_set_profiling(ys_context* c, int32_t on) {
 int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
   return guarded(c, [&] {
     for (int k = 0; k < 7; ++k) ms[k] = c->stage_ms[k];
-    for (int k = 0; k < 4; ++k) ms[8 + k] = c->pcg_phase_ms[k];
+    for (int k = 0; k < 8; ++k) ms[8 + k] = c->pcg_phase_ms[k];
     if (counts) {
       counts[0] = c->launches;
       int64_t evd = 0;
@@ -1014,6 +1015,7 @@ int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
         for (unsigned v : h) evd += v;
       }
       counts[1] = evd;  // indefinite 9x9 projections (EVD pass) in the last assembly
+      counts[2] = c->pcg_path;
     }
   });
 }
@@ -1206,6 +1208,10 @@ int ys_dist_info(ys_context* c, int32_t* rank, int32_t* nranks, int64_t* bounds,
 
 int ys_stream(ys_context* c, void** stream) {
   return guarded(c, [&] { *stream = reinterpret_cast<void*>(c->stream); });
+}
+
+int ys_pcg_layout_info(ys_context* c, int64_t* info, int64_t* cta) {
+  return guarded(c, [&] { sym_info(*c, info, cta); });
 }
 
 int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <chrono>
 
+#include "ys_grid.cuh"
 #include "ys_sell.cuh"
 
 namespace ys {
@@ -479,94 +480,6 @@ __global__ void k_pupdate(int64_t s, const double* __restrict__ z, double* __res
 // separated by a grid barrier; after each barrier every CTA reduces the same
 // per-CTA partials in the same fixed order, so all CTAs hold bit-identical
 // alpha / beta / status without a last-CTA round trip (deterministic).
-struct GridBar {
-  unsigned int count;  // generation barrier
-  unsigned int gen;
-  unsigned long long arrivals;  // counter barrier: only grows within a launch
-};
-
-__device__ __forceinline__ void grid_sync(GridBar* gb) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = &gb->gen;
-    const unsigned int g = *vgen;
-    __threadfence();
-    if (atomicAdd(&gb->count, 1u) == gridDim.x - 1) {
-      gb->count = 0;
-      __threadfence();
-      atomicAdd(&gb->gen, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Counter barrier: one red.release (no return value) per CTA on a counter
-// that only grows, then acquire-polling until it reaches G * epoch.  The
-// release orders this CTA's writes before its arrival; the acquire load orders
-// the poller's later reads after every arrival (and invalidates L1).  No
-// returning atomic is serialised at one address and no generation word is
-// needed; the counter is zeroed before each launch.
-__device__ __forceinline__ void grid_sync_counter(unsigned long long* count, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
-    unsigned long long v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
-      if (v >= target) break;
-      __nanosleep(32);
-    }
-  }
-  __syncthreads();
-}
-
-// The counter barrier split in two: arrive (every thread's prior writes
-// ordered before the CTA's release-add) and wait (acquire poll), so a CTA can
-// issue loads that do not depend on other CTAs' writes in between.
-__device__ __forceinline__ void grid_arrive(unsigned long long* count) {
-  __syncthreads();
-  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
-}
-
-__device__ __forceinline__ void grid_wait(unsigned long long* count, unsigned long long target) {
-  if (threadIdx.x == 0) {
-    unsigned long long v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
-      if (v >= target) break;
-      __nanosleep(32);
-    }
-  }
-  __syncthreads();
-}
-
-// Fixed-order sum of n partials (stride between the K arrays = n) inside every CTA.
-template <int K>
-__device__ __forceinline__ void reduce_partials_all(const double* part, int n, double (&out)[K]) {
-  __shared__ double res[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = 0.0;
-  for (int q = threadIdx.x; q < n; q += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < K; ++k) out[k] += __ldcg(part + k * n + q);
-  block_reduce<K>(out);
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int k = 0; k < K; ++k) res[k] = out[k];
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = res[k];
-  __syncthreads();
-}
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 // SH = 0: row gather from upper storage (ys_spmv.cuh); SH > 0: the sliced-ELL
 // full copy with SH lanes per block row (ys_sell.cuh).
@@ -1344,15 +1257,13 @@ void drop_pcg_graph(Context& c) {
 
 int pcg_grid(Context& c) { return std::max(1, sm_count() * 8); }
 
-// The layout half of the uniform-3x3 solve's sliced-ELL build (sell_prepare),
-// when the next ctx_pcg will take that path.
+// The layout half of the uniform-3x3 solve's copy of H (the symmetric band
+// copy, ys_sym.cu), when the next ctx_pcg will take that path: built right
+// after the dynamic rebuild, while the static evaluation runs on the side streams.
 void pcg_prepare(Context& c) {
   const bool has1 = c.S[1].n_blocks > 0;
   const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
-  const char* pe = getenv("YS_PCG_PERSISTENT");
-  const char* se = getenv("YS_PCG_SELL");
-  if (!fast || (pe && std::string(pe) == "0") || (se && atoi(se) != 4)) return;
-  sell_prepare(c, 4);
+  if (fast) sym_prepare(c);
 }
 
 void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev, ys_step_stats* stats) {
@@ -1377,31 +1288,26 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
                                   c.pcg.p, c.partials.p, c.hist.p);
   YS_LAUNCH_CHECK();
 
-  // Uniform 3x3 systems: one persistent cooperative kernel runs the whole solve.
+  // Uniform 3x3 systems: one persistent cooperative kernel runs the whole solve,
+  // over the symmetric band copy (ys_sym.cu); when its layout does not fit
+  // the shared memory, over the sliced-ELL full copy, and when that plan does
+  // not fit either, the row gather from upper storage.  The path taken is
+  // reported (ys_stage_times, "pcg_path").
   {
     const bool has1 = c.S[1].n_blocks > 0;
     const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
-    static const bool persistent_off = getenv("YS_PCG_PERSISTENT") && std::string(getenv("YS_PCG_PERSISTENT")) == "0";
-    if (fast && !persistent_off) {
-      // YS_PCG_SELL: lanes per block row of the sliced-ELL copy (0: row gather
-      // from upper storage).
-      static const int sell_h = [] {
-        const char* e = getenv("YS_PCG_SELL");
-        return e ? atoi(e) : 4;
-      }();
-      if (sell_h != 0 && sell_h != 1 && sell_h != 2 && sell_h != 4)
-        fail(YS_ERR_VALIDATION, "YS_PCG_SELL must be 0, 1, 2 or 4");
-      if (sell_h > 0 && sell_h != 4) sell_build(c, sell_h);
-      SellDev sl = sell_dev(c);
+    if (fast) {
       int64_t nb = c.NB;
       const double* minv = c.minv.p;
       double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *hist = c.hist.p;
       PcgState* stp = c.pcg.p;
+      static const bool sym_off = getenv("YS_EXPERIMENT_SELL") != nullptr;  // temporary A/B switch
+      bool launched = !sym_off && sym_pcg(c, stats);
+      if (launched) c.pcg_path = 1;
       c.gridbar.resize(sizeof(GridBar));
-      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
-      bool launched = false;
-      if (sell_h == 4 && !launched) {
+      if (!launched) {
+        YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
         // full sliced-ELL copy, per-warp plan cache in shared memory
         sell_build(c, 4);
         SellDev sl = sell_dev(c);
@@ -1430,14 +1336,12 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
           void* args[] = {&A, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
           YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, smem, s));
           launched = true;
+          c.pcg_path = 2;
         }
       }
       if (!launched) {
-        void* kern = sell_h == 0   ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 0>)
-                     : sell_h == 1 ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 1>)
-                     : sell_h == 2 ? reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 2>)
-                                   : reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 4>);
-        // 256 x 3 CTAs per SM (384 x 2, the same 768 threads, measured equal at C5)
+        // row gather from upper storage (no copy, no shared-memory plan)
+        void* kern = reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 0>);
         int occ = 0;
         YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
         if (occ < 1) occ = 1;
@@ -1445,16 +1349,19 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         c.partials.resize(std::max<size_t>(c.partials.n, size_t(3 * gsz)));
         SpmvDev d0 = spmv_dev(c.S[0]);
         SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+        SellDev sl{};
         int h1 = has1 ? 1 : 0;
         double* part = c.partials.p;
         void* args[] = {&d0, &d1, &sl, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
         YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
+        c.pcg_path = 3;
       }
       PcgState fin{};
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
       c.launches += 2;
       for (int k = 0; k < 4; ++k) c.pcg_phase_ms[k] = double(fin.phase_ns[k]) * 1e-6;
+      for (int k = 0; k < 4; ++k) c.pcg_phase_ms[4 + k] = double(fin.aux_ns[k]) * 1e-6;
       c.hist_count = fin.status == 1 && fin.it == 0 && fin.gnorm == 0.0 ? 0 : fin.it + 1;
       if (fin.status == 3)
         fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +
@@ -1515,6 +1422,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       YS_CUDA(cudaStreamSynchronize(s));
       c.launches += 2;
       for (int k = 0; k < 4; ++k) c.pcg_phase_ms[k] = double(fin.phase_ns[k]) * 1e-6;
+      for (int k = 0; k < 4; ++k) c.pcg_phase_ms[4 + k] = double(fin.aux_ns[k]) * 1e-6;
       c.hist_count = fin.status == 1 && fin.it == 0 && fin.gnorm == 0.0 ? 0 : fin.it + 1;
       if (fin.status == 3)
         fail(YS_ERR_NUMERICAL, "PCG diverged at iteration " + std::to_string(fin.fail_it) +

@@ -497,14 +497,33 @@ class Engine:
         self._c(self.f["stream"](self.ctx, C.byref(h)))
         return h.value or 0
 
+    def pcg_path(self) -> str:
+        """Kernel path of the last uniform-3x3 solve."""
+        ms = np.zeros(16)
+        cnt = np.zeros(3, dtype=np.int64)
+        self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
+        return {1: "symmetric band copy", 2: "sliced-ELL copy", 3: "row gather"}.get(int(cnt[2]), "general")
+
+    def pcg_layout_info(self, per_cta: bool = False):
+        """Sizes of the last symmetric band copy (and per-CTA clocks of its solve)."""
+        info = np.zeros(12, dtype=np.int64)
+        cta = np.zeros(8 * 1024, dtype=np.int64)
+        self._c(self.f["pcg_layout_info"](self.ctx, _ip64(info), _ip64(cta)))
+        keys = ["ctas", "tiles", "max_rows", "window", "stages", "stage_bytes", "max_blocks_per_tile", "near",
+                "far", "spill_slots", "smem", "usable"]
+        d = dict(zip(keys, info.tolist()))
+        if per_cta:
+            d["cta"] = cta[:8 * d["ctas"]].reshape(-1, 8)
+        return d
+
     def time_kernel(self, which: int, reps: int = 20):
         ms, b = C.c_double(), C.c_double()
         self._c(self.f["time_kernel"](self.ctx, which, reps, C.byref(ms), C.byref(b)))
         return ms.value, b.value
 
     def stage_times(self, with_counts: bool = False):
-        ms = np.zeros(12)
-        cnt = np.zeros(2, dtype=np.int64)
+        ms = np.zeros(16)
+        cnt = np.zeros(3, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
         if with_counts:
             return ms, int(cnt[0]), int(cnt[1])

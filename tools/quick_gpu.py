@@ -34,6 +34,6 @@ for name in names:
           f"step_ms={[round(1e3*t,2) for t in times]} pcg_it={st.pcg_iterations} conv={st.pcg_converged} "
           f"res={st.pcg_residual:.2e} stages(ms) refresh={ms[0]:.3f} eval={ms[1]:.3f} gather={ms[2]:.3f} "
           f"rows={ms[3]:.3f} pcg={ms[4]:.3f} total={ms[6]:.3f} launches={launches} evd={nevd} "
-          f"pcg_phases(ms)={[round(v, 2) for v in ms[8:12]]}", flush=True)
+          f"pcg_phases(ms)={[round(v, 2) for v in ms[8:12]]} path={eng.pcg_path()} aux={[round(v, 3) for v in ms[12:16]]}", flush=True)
     print(f"   spmv {sp_ms*1e3:.1f}us {sp_b/sp_ms/1e6:.0f} GB/s | assembly {as_ms*1e3:.1f}us {as_b/as_ms/1e6:.0f} GB/s | "
           f"eval {ev_ms*1e3:.1f}us | dev bytes {eng.device_bytes()/1e9:.2f} GB", flush=True)
