@@ -28,6 +28,17 @@ import time
 
 import numpy as np
 
+
+def simulation(cfg, backend: str = "gpu", **kw):
+    """The product Simulation on the B200 library; backend "oracle" injects the
+    CPU oracle (test infrastructure: the CPU baseline / reference arm only)."""
+    from paper_2605_23088_b200.scene import Simulation
+    lib = None
+    if backend == "oracle":
+        import oracle
+        lib = oracle.library()
+    return Simulation(cfg, library=lib, **kw)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -73,9 +84,9 @@ def prepare(name: str, via_f: bool, backend: str, device: int = 0):
     """Scene + prepared state: seeded jitter of the soft vertices, x_tilde of
     frame 1 (begin_frame), contact pairs of that state."""
     from paper_2605_23088_b200 import configs
-    from paper_2605_23088_b200.scene import SimConfig, Simulation
+    from paper_2605_23088_b200.scene import SimConfig
     cfg = SimConfig.from_dict(scene_config(name, via_f))
-    sim = Simulation(cfg, backend=backend, device=device, refresh_pairs=False)
+    sim = simulation(cfg, backend, device=device, refresh_pairs=False)
     configs.jitter_targets(sim, jitter_amplitude(name))
     sim.begin_frame()
     sim.refresh_dynamic_pairs()
@@ -146,7 +157,7 @@ def cpu_sample(name: str, via_f: bool, gpu_pcg_iterations: int, budget_s: float 
     parallel_for, the oracle evaluates instances on all host threads
     (YO_THREADS caps them) and scatters / iterates serially."""
     from paper_2605_23088_b200 import configs
-    from paper_2605_23088_b200.scene import SimConfig, Simulation
+    from paper_2605_23088_b200.scene import SimConfig
     backend, kind = "oracle", "port"
     full = scene_config(name, via_f)
     sub = dict(full)
@@ -154,7 +165,7 @@ def cpu_sample(name: str, via_f: bool, gpu_pcg_iterations: int, budget_s: float 
     sub["bodies"] = [soft[0]] + [b for b in full["bodies"] if b.get("fixed")]
     sub["contact"] = dict(full["contact"], bodies=[soft[0]["name"]] + [b["name"] for b in full["bodies"] if b.get("fixed")])
     cfg = SimConfig.from_dict(sub)
-    sim = Simulation(cfg, backend=backend, refresh_pairs=False)
+    sim = simulation(cfg, backend, refresh_pairs=False)
     configs.jitter_targets(sim, jitter_amplitude(name))
     sim.begin_frame()
     sim.refresh_dynamic_pairs()
@@ -262,7 +273,7 @@ def main():
     eng.set_profiling(False)
 
     peak, peak_src = load_peaks()
-    spmv_ms, spmv_bytes = eng.time_kernel(42, 50)  # the PCG's SpMV: sliced-ELL copy, 4 lanes per row
+    spmv_ms, spmv_bytes = eng.time_kernel(3, 50)  # the PCG's SpMV: sliced-ELL copy, 4 lanes per row
     asm_ms, asm_bytes = eng.time_kernel(1, 10)
     eval_ms, _ = eng.time_kernel(2, 5)
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9

@@ -259,8 +259,8 @@ int ys_dist_info(ys_context* ctx, int32_t* rank, int32_t* nranks, int64_t* bound
  * [5] SpMV (sum over iterations), [6] total; [8..11] persistent-PCG phase clocks,
  * [12..15] its sub-phase clocks (ms must hold 16 doubles).
  * counts[0] = kernel launches, counts[1] = indefinite 9x9 projections of the
- * last assembly, counts[2] = uniform-3x3 PCG path of the last solve (1 symmetric
- * band copy, 2 sliced-ELL copy, 3 row gather; 0 other).
+ * last assembly, counts[2] = uniform-3x3 PCG path of the last solve (1 sliced-ELL
+ * copy, 2 row gather from upper storage; 0 other).
  * ------------------------------------------------------------------------ */
 int ys_set_profiling(ys_context* ctx, int32_t enabled);
 int ys_stage_times(ys_context* ctx, double* ms, int64_t* counts);
@@ -270,18 +270,18 @@ int ys_bump_dynamic_epoch(ys_context* ctx);
 /* The cudaStream_t every kernel of the context is launched on (for CUDA-event
  * timing by the caller). */
 int ys_stream(ys_context* ctx, void** stream);
+/* Execution options (no effect on results): "overlap" (default 1) evaluates the
+ * static energies on side streams while minimize_step rebuilds the dynamic
+ * group; 0 runs the stages sequentially (bitwise the same step). */
+int ys_set_option(ys_context* ctx, const char* name, int64_t value);
 /* Times one kernel class alone: reps launches bracketed by CUDA events on the
- * context stream.  which: 0 = PCG SpMV (static + dynamic, fused pHp),
- * 1 = assembly gather of the static group, 2 = local evaluation of all
- * energies.  avg_ms per launch; bytes = algorithmic bytes per launch. */
+ * context stream.  which: 0 = SpMV row gather from upper storage (static +
+ * dynamic), 1 = assembly gather + gradient / diagonal / preconditioner rows,
+ * 2 = local evaluation of all energies, 3 = the PCG's SpMV through the
+ * sliced-ELL copy (uniform 3x3 systems).  avg_ms per launch; bytes =
+ * algorithmic bytes per launch. */
 int ys_time_kernel(ys_context* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);
-/* Layout of the last symmetric band copy (uniform-3x3 PCG, ys_sym.cu): info[0..11] =
- * CTAs, tiles, max rows per CTA, window rows, ring stages, stage bytes, blocks
- * per tile (max), near blocks, far blocks, spill slots, shared bytes, usable.
- * cta (optional, CTAs x 8) = per-CTA clocks of the last solve: far blocks,
- * tile waits, tile work, phase-B spills, phase-B update (cycles, summed over
- * iterations), rows, far blocks, spill slots. */
-int ys_pcg_layout_info(ys_context* ctx, int64_t* info, int64_t* cta);
+
 
 #ifdef __cplusplus
 }

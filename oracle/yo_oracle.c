@@ -2220,6 +2220,14 @@ int yo_stream(yo_context* c, void** stream) {
   API_END;
 }
 
+/* Execution options (ys_set_option): the oracle is sequential, "overlap" has no effect. */
+int yo_set_option(yo_context* c, const char* name, int64_t value) {
+  API_BEGIN(c);
+  (void)value;
+  if (!name || strcmp(name, "overlap") != 0) fail(c, YS_ERR_VALIDATION, "unknown option '%s'", name ? name : "");
+  API_END;
+}
+
 /* --- free-standing BSR ---------------------------------------------------- */
 int yo_bsr_build(yo_context* c, int64_t s, int64_t n, const int64_t* coords, int32_t* id) {
   API_BEGIN(c);

@@ -1,9 +1,9 @@
 """ctypes binding of the C-ABI declared in include/yasps_b200.h.
 
-The same signatures are exported by the B200 library (prefix ``ys_``) and by
-the CPU oracle under oracle/ (prefix ``yo_``, test infrastructure only).  The
-product path loads ``libyasps_b200.so`` and raises if it is missing — there is
-no CPU fallback.
+The product loads ``libyasps_b200.so`` (prefix ``ys_``) and raises if it is
+missing — there is no CPU fallback.  ``Library`` binds any implementation of
+the same ABI; the test infrastructure under oracle/ uses it for the CPU oracle
+(``yo_``) and injects it into ``Engine`` — the product never loads it.
 """
 from __future__ import annotations
 
@@ -134,8 +134,8 @@ _SIGS = {
     "stage_times": [_P, _PD, _PI64],
     "bump_dynamic_epoch": [_P],
     "stream": [_P, C.POINTER(C.c_void_p)],
+    "set_option": [_P, C.c_char_p, _I64],
     "time_kernel": [_P, _I32, _I32, _PD, _PD],
-    "pcg_layout_info": [_P, _PI64, _PI64],
     "dist_unique_id": [C.c_char_p],
     "dist_init_nccl": [_P, _I32, _I32, C.c_char_p],
     "dist_init_host": [_P, _I32, _I32, ALLGATHER_FN, _P],
@@ -145,7 +145,7 @@ _SIGS = {
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
-OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "pcg_layout_info", "stream", "dist_unique_id",
+OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream", "set_option", "dist_unique_id",
             "dist_init_nccl"}
 
 
@@ -187,20 +187,6 @@ def gpu_library() -> Library:
     if "gpu" not in _LIBS:
         _LIBS["gpu"] = Library(LIB_PATH, "ys_")
     return _LIBS["gpu"]
-
-
-def oracle_library() -> Library:
-    """CPU restatement (test infrastructure; imported only by tests / smoke / bench baseline)."""
-    if "oracle" not in _LIBS:
-        _LIBS["oracle"] = Library(ROOT / "oracle" / "liboracle.so", "yo_")
-    return _LIBS["oracle"]
-
-
-def reference_library() -> Library:
-    """The reference relsim compiled from /root/reference against eigen-lite (oracle/_ref)."""
-    if "ref" not in _LIBS:
-        _LIBS["ref"] = Library(ROOT / "oracle" / "_ref" / "librelsim_capi.so", "yr_")
-    return _LIBS["ref"]
 
 
 def check(lib: Library, ctx, status: int):

@@ -773,12 +773,12 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
   c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * evd_total)));
   c.evd_list.resize(std::max(c.evd_list.n, size_t(evd_total)));
   const bool pass_b = with_hessian && project;
-  // pass B (Jacobi EVD of the indefinite elements) can run batched over
-  // pending stencil energies of one kind (YS_EVD_BATCH = elements per batch).
-  // Default: right after each energy's pass A, while its M buffer (360 B per
-  // indefinite element) sits in L2.  C5 (8 bodies of 127k tets), eval stage:
-  // per energy 4.93 ms, batches of 2 bodies 5.0, 4 bodies 5.4, all 8 6.4 ms.
-  static const int64_t kBatchElems = getenv("YS_EVD_BATCH") ? atoll(getenv("YS_EVD_BATCH")) : 1;
+  // pass B (Jacobi EVD of the indefinite elements) runs right after each
+  // energy's pass A, while its M buffer (360 B per indefinite element) sits in
+  // L2 (batching pass B over several bodies was measured slower: C5 eval stage
+  // per energy 4.93 ms, batches of 2 bodies 5.0, 4 bodies 5.4, all 8 6.4 ms);
+  // many small energies of one kind still share a launch.
+  constexpr int64_t kBatchElems = 1;
   const unsigned gb = unsigned(sm_count() * 4);
   std::vector<size_t> pending;
   int pending_kind = -1;

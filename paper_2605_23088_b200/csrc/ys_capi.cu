@@ -50,8 +50,6 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
                  PcgState* st, double* part, int grid);
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
-bool spmv_variant(Context& c, int v, const double* x, double* y);
-void barrier_probe(Context& c, int n, int with_reduce);
 
 
 namespace {
@@ -761,18 +759,6 @@ int ys_apply_hessian(ys_context* c, const double* x, double* y) {
     c->hp.resize(c->s + 2);
     YS_CUDA(cudaMemcpyAsync(c->r.p, x, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     YS_CUDA(cudaMemcpyAsync(c->hp.p, y, c->s * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    static const int variant = getenv("YS_APPLY_VARIANT") ? atoi(getenv("YS_APPLY_VARIANT")) : 0;
-    if (variant >= 40 && variant < 44 && c->uniform3) {
-      // diagnostic: y += H x through the sliced-ELL copy with 2^(variant-40) lanes per row
-      sell_build(*c, 1 << (variant - 40));
-      c->z.resize(c->s + 2);
-      spmv_sell(*c, c->r.p, c->z.p);
-      std::vector<double> t(c->s);
-      YS_CUDA(cudaMemcpyAsync(t.data(), c->z.p, c->s * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-      YS_CUDA(cudaStreamSynchronize(c->stream));
-      for (int64_t i = 0; i < c->s; ++i) y[i] += t[i];
-      return;
-    }
     ctx_apply_hessian_dev(*c, c->r.p, c->hp.p);
     YS_CUDA(cudaMemcpyAsync(y, c->hp.p, c->s * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     YS_CUDA(cudaStreamSynchronize(c->stream));
@@ -785,13 +771,13 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     auto t0 = std::chrono::steady_clock::now();
     c->launches = 0;
     c->sell_prepared = false;
-    c->sym.prepared = false;
     if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
     // The static energies' evaluation (SNH, inertia: nearly all of the local
     // work) does not depend on the dynamic structure: it runs on a second
     // stream while the dynamic group is rebuilt (whose host synchronisations
-    // would otherwise leave the device idle).  YS_OVERLAP=0: sequential.
-    static const bool overlap = !(getenv("YS_OVERLAP") && std::string(getenv("YS_OVERLAP")) == "0");
+    // would otherwise leave the device idle); ys_set_option("overlap", 0):
+    // sequential (bitwise the same step, tested).
+    const bool overlap = c->overlap;
     bool dyn_stencil = false;
     for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
     if (overlap && !dyn_stencil) {
@@ -1206,12 +1192,16 @@ int ys_dist_info(ys_context* c, int32_t* rank, int32_t* nranks, int64_t* bounds,
   });
 }
 
-int ys_stream(ys_context* c, void** stream) {
-  return guarded(c, [&] { *stream = reinterpret_cast<void*>(c->stream); });
+int ys_set_option(ys_context* c, const char* name, int64_t value) {
+  return guarded(c, [&] {
+    const std::string n = name ? name : "";
+    if (n == "overlap") c->overlap = value != 0;
+    else fail(YS_ERR_VALIDATION, "unknown option '" + n + "'");
+  });
 }
 
-int ys_pcg_layout_info(ys_context* c, int64_t* info, int64_t* cta) {
-  return guarded(c, [&] { sym_info(*c, info, cta); });
+int ys_stream(ys_context* c, void** stream) {
+  return guarded(c, [&] { *stream = reinterpret_cast<void*>(c->stream); });
 }
 
 int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
@@ -1221,25 +1211,24 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
     cudaStream_t s = c->stream;
     double alg = 0.0;
     auto launch = [&]() {
-      if (which >= 40 && which < 48) {
-        // sliced-ELL copy of the PCG: SpMV 40-43 (H = 1, 2, 4, 8 lanes per row), its build 44-47
-        if (which >= 44) sell_build(*c, 1 << (which - 44));
-        else spmv_sell(*c, c->p.p, c->hp.p);
-      } else if (which == 5 || which == 6) {  // 1000 counter grid barriers per launch (6: + partial reductions)
-        barrier_probe(*c, 1000, which == 6 ? 3 : 2);
-      } else if (which >= 10) {
-        if (!spmv_variant(*c, which - 10, c->p.p, c->hp.p)) fail(YS_ERR_VALIDATION, "unknown SpMV variant");
+      if (which == 3) {
+        spmv_sell(*c, c->p.p, c->hp.p);  // the PCG's SpMV: the sliced-ELL copy, 4 lanes per row
       } else if (which == 0) {
         spmv_launch(*c, c->S[0], &c->S[1], c->p.p, c->hp.p, false, nullptr, nullptr, pcg_grid(*c));
       } else if (which == 1) {
         ctx_gather_all(*c);
         ctx_block_rows(*c, true);
-      } else {
+      } else if (which == 2) {
         ctx_eval_all(*c, true, true);
+      } else {
+        fail(YS_ERR_VALIDATION, "ys_time_kernel: unknown kernel class");
       }
     };
-    if (which >= 40 && which < 44) sell_build(*c, 1 << (which - 40));
-    if (which == 0 || which >= 10) {
+    if (which == 3) {
+      if (!c->uniform3) fail(YS_ERR_VALIDATION, "ys_time_kernel(3): the sliced-ELL copy needs uniform 3x3 blocks");
+      sell_build(*c, 4);
+    }
+    if (which == 0 || which == 3) {
       c->p.resize(c->s + 2);
       c->hp.resize(c->s + 2);
       YS_CUDA(cudaMemcpyAsync(c->p.p, c->G.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, s));

@@ -229,39 +229,7 @@ struct Context {
   int64_t sell_rows = 0, sell_slices = 0;  // entry rows, slices
   int64_t sell_r0 = 0, sell_r1 = 0;         // block-row range of the copy
 
-  // symmetric band copy of H_static + H_dynamic for the uniform 3x3 PCG
-  // (ys_sym.cu): upper blocks once, CTA-owned row ranges, tiles staged by bulk
-  // copies, transposed products accumulated on chip
-  struct Sym {
-    bool prepared = false;  // layout built for the current structures
-    bool usable = false;    // the layout fits the kernel's shared memory
-    int G = 0, ntiles = 0, max_range = 0, W = 0, nstages = 0, stage_bytes = 0, em = 0;
-    size_t smem = 0;
-    int64_t nnear = 0, H = 0, nspill = 0;
-    DevBuf<int32_t> eoff;          // NB + 1: static work per row, scanned
-    DevBuf<int32_t> enoff, hoff;   // NB + 1: near blocks / half-entries per row, scanned
-    DevBuf<int32_t> range;         // G + 1: block-row bounds of the CTAs
-    DevBuf<int32_t> tflag;         // NB + 1: tile starts, scanned to tile ids
-    DevBuf<int32_t> trow0;         // ntiles + 1: first block row of each tile
-    DevBuf<int32_t> ctile;         // G + 1: first tile of each CTA
-    DevBuf<int32_t> tcta;          // ntiles: owning CTA
-    DevBuf<int32_t> tns;           // ntiles + 1: spill targets per tile, scanned to producer bases
-    DevBuf<int32_t> tsize;         // ntiles: bytes of each tile image
-    DevBuf<int64_t> toff;          // ntiles: byte offset of each tile image
-    DevBuf<unsigned char> blob;    // tile images
-    DevBuf<unsigned long long> hkey, hkey_s;  // half-entries: (target, position) keys
-    DevBuf<uint32_t> hpay, hpay_s;            // block | group | transposed
-    DevBuf<int32_t> htgt, hsrc, hslot, hrid;  // sorted: target, source block row, slot, run heads scanned
-    DevBuf<int32_t> cbase;         // G + 1: first half-entry chunk of each CTA
-    DevBuf<uint32_t> runs;         // chunks x kSymChunk: run start | length | flags
-    DevBuf<int32_t> rslot, nruns;  // chunks x kSymChunk slots; runs per chunk
-    DevBuf<double> hval;           // 9 oriented values per half-entry
-    DevBuf<int32_t> spill_c, spill_cs, spill_o, spill_os, spill_ptr;
-    DevBuf<double> spill_val;      // 3 per slot
-    DevBuf<int64_t> summary;       // device-side sizes read back by the layout
-    DevBuf<int64_t> clocks;        // G x 8 per-CTA clocks of the last solve
-  } sym;
-  int pcg_path = 0;  // last uniform-3x3 solve: 1 symmetric band kernel, 2 sliced-ELL copy (fallback)
+  int pcg_path = 0;  // last uniform-3x3 solve: 1 sliced-ELL copy, 2 row gather (the copy's plan does not fit)
 
   // structure-build scratch (reused across dynamic rebuilds)
   DevBuf<unsigned char> cubtmp;
@@ -283,6 +251,7 @@ struct Context {
 
   // profiling
   bool profiling = false;
+  bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
   double stage_ms[8] = {0};
   double pcg_phase_ms[8] = {0};
   int64_t launches = 0;
@@ -341,9 +310,6 @@ void drop_pcg_graph(Context& c);
 void sell_build(Context& c, int lanes_per_row, int64_t r0 = 0, int64_t r1 = -1);  // ys_sell.cu
 void sell_prepare(Context& c, int lanes_per_row, int64_t r0 = 0, int64_t r1 = -1);  // ys_sell.cu
 void pcg_prepare(Context& c);  // ys_solver.cu
-void sym_prepare(Context& c);  // ys_sym.cu: layout of the symmetric band copy
-bool sym_pcg(Context& c, ys_step_stats* stats);  // ys_sym.cu: false if the layout does not fit
-void sym_info(Context& c, int64_t* info, int64_t* cta);  // ys_sym.cu: layout sizes, per-CTA clocks
 void spmv_sell(Context& c, const double* x, double* y);
 int sell_max_warp_rows(Context& c, int64_t warps, int slices_per_warp);   // y = H x through the sliced-ELL copy
 bool pcg_uses_conditional_graph(Context& c);

@@ -185,47 +185,6 @@ __global__ void k_copy_rows(const double* __restrict__ x, int64_t r0, int64_t r1
 // ---------------------------------------------------------------------------
 // Solver kernels over the owned rows [r0, r1); rank partials -> out.
 
-__global__ void __launch_bounds__(kTB, kSpmvMinB) k_dspmv33(SpmvDev S0, SpmvDev S1, int has1, int64_t r0, int64_t r1,
-                                                    const double* __restrict__ x, double* __restrict__ y,
-                                                    PcgState* st, double* part, double* out) {
-  constexpr int SW = kSpmvSW;
-  if (st->status) return;
-  const int lane = threadIdx.x % SW;
-  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
-  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
-  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
-  double dot[1] = {0.0};
-  for (int64_t R = r0 + sw0; R < r1; R += nsw) {
-    const RowPtrs p0 = load_rowptrs(S0, R);
-    RowPtrs p1{0, 0, 0, 0};
-    if (has1) p1 = load_rowptrs(S1, R);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33_u2<SW>(S0, p0, lane, x, a0, a1, a2);
-    if (has1) acc33_u2<SW>(S1, p1, lane, x, a0, a1, a2);
-#pragma unroll
-    for (int off = SW / 2; off > 0; off >>= 1) {
-      a0 += __shfl_xor_sync(mask, a0, off, SW);
-      a1 += __shfl_xor_sync(mask, a1, off, SW);
-      a2 += __shfl_xor_sync(mask, a2, off, SW);
-    }
-    if (lane == 0) {
-      double* yo = y + 3 * R;
-      yo[0] = a0;
-      yo[1] = a1;
-      yo[2] = a2;
-      dot[0] += x[3 * R] * a0 + x[3 * R + 1] * a1 + x[3 * R + 2] * a2;
-    }
-  }
-  block_reduce<1>(dot);
-  if (threadIdx.x == 0) part[blockIdx.x] = dot[0];
-  if (!last_cta(&st->counter1)) return;
-  double tot[1];
-  sum_partials<1>(part, gridDim.x, 0, tot);
-  if (threadIdx.x == 0) {
-    st->counter1 = 0;
-    out[0] = tot[0];
-  }
-}
 
 // The same over the sliced-ELL copy of the owned rows (sell_build(c, 4, r0,
 // r1): every block touching an owned row, stored for that row): coalesced
@@ -544,23 +503,16 @@ void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats
   k_dinit_fin<<<1, 1, 0, s>>>(st, d.dall.p, n, c.hist.p);
   YS_LAUNCH_CHECK();
 
-  // the owned rows' sliced-ELL copy (YS_DIST_SPMV=rowgather: the upper-storage row gather)
-  static const bool row_gather = getenv("YS_DIST_SPMV") && std::string(getenv("YS_DIST_SPMV")) == "rowgather";
-  SpmvDev d0 = spmv_dev(c.S[0]);
-  SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
-  if (!row_gather) sell_build(c, 4, r0, r1);
+  // the owned rows' sliced-ELL copy
+  sell_build(c, 4, r0, r1);
   SellDev sl = sell_dev(c);
-  static int occ = 0, occ_sell = 0;
-  if (!occ) {
-    YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dspmv33, kTB, 0));
+  static int occ_sell = 0;
+  if (!occ_sell) {
     YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sell, k_dspmv_sell, kTB, 0));
-    occ = std::max(occ, 1);
     occ_sell = std::max(occ_sell, 1);
   }
-  const int sg = row_gather
-                     ? int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(4 * (r1 - r0), kTB), int64_t(occ) * sm_count())))
-                     : int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(32 * sl.nslices, kTB),
-                                                                  int64_t(occ_sell) * sm_count())));
+  const int sg = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(32 * sl.nslices, kTB),
+                                                            int64_t(occ_sell) * sm_count())));
   auto iteration = [&] {
     if (d.max_exp > 0) {
       k_pack<<<blocks_for(3 * my_exp), kTB, 0, s>>>(c.p.p, d.exp.p + d.exp_off[me], my_exp, d.send.p, st);
@@ -568,10 +520,7 @@ void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats
       k_unpack<<<blocks_for(3 * total_exp), kTB, 0, s>>>(d.recv.p, d.exp.p, d.dexp_off.p, n, me, d.max_exp, total_exp,
                                                          c.p.p, st);
     }
-    if (row_gather)
-      k_dspmv33<<<sg, kTB, 0, s>>>(d0, d1, has1 ? 1 : 0, r0, r1, c.p.p, c.hp.p, st, part, d.dsend.p);
-    else
-      k_dspmv_sell<<<sg, kTB, 0, s>>>(sl, c.p.p, c.hp.p, st, part, d.dsend.p);
+    k_dspmv_sell<<<sg, kTB, 0, s>>>(sl, c.p.p, c.hp.p, st, part, d.dsend.p);
     allgather(c, d.dsend.p, d.dall.p, 1);
     k_dalpha<<<1, 1, 0, s>>>(st, d.dall.p, n);
     k_dupdate<<<vg, kTB, 0, s>>>(c.minv.p, c.DX.p, c.r.p, c.z.p, c.p.p, c.hp.p, r0, r1, st, part, d.dsend.p);

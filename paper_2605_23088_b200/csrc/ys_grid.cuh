@@ -1,5 +1,5 @@
 // ys_grid.cuh — grid-wide synchronisation of the persistent cooperative PCG
-// kernels (ys_solver.cu, ys_sym.cu): counter barriers, fixed-order reductions
+// kernels (ys_solver.cu): counter barriers, fixed-order reductions
 // of the per-CTA partials (every CTA sums them in the same order, so alpha /
 // beta / status are bit-identical everywhere without a last-CTA round trip),
 // and the %globaltimer phase clock.

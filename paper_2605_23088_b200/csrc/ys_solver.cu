@@ -90,131 +90,6 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_spmv33(SpmvDev S0, SpmvDev S
   }
 }
 
-// Diagnostic variants of the 3x3 SpMV (YS_SPMV_VARIANT): register caps and
-// partial work, used to attribute the kernel's time (not used by PCG).
-template <int SW, int MINB, int PART, bool PREF>
-__global__ void __launch_bounds__(kTB, MINB) k_spmv33_var(SpmvDev S0, int64_t nb, const double* __restrict__ x,
-                                                          double* __restrict__ y) {
-  const int lane = threadIdx.x % SW;
-  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
-  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
-  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
-  RowPtrs nxt{};
-  if (PREF && sw0 < nb) nxt = load_rowptrs(S0, sw0);
-  for (int64_t R = sw0; R < nb; R += nsw) {
-    RowPtrs rp;
-    if (PREF) {
-      rp = nxt;
-      if (R + nsw < nb) nxt = load_rowptrs(S0, R + nsw);
-    } else {
-      rp = load_rowptrs(S0, R);
-    }
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    if (PART != 2)
-      for (int32_t u = rp.n0 + lane; u < rp.n1; u += SW) {
-        double v[9];
-        load_block9(S0.values + 9 * int64_t(u), v);
-        double x0 = 1.0, x1 = 1.0, x2 = 1.0;
-        if (PART != 3) load_vec3(x + S0.col[u], x0, x1, x2);
-        a0 += v[0] * x0 + v[1] * x1 + v[2] * x2;
-        a1 += v[3] * x0 + v[4] * x1 + v[5] * x2;
-        a2 += v[6] * x0 + v[7] * x1 + v[8] * x2;
-      }
-    if (PART != 1)
-      for (int32_t j = rp.t0 + lane; j < rp.t1; j += SW) {
-        const int2 t = S0.tlist[j];
-        double v[9];
-        load_block9(S0.values + 9 * int64_t(t.x), v);
-        double x0 = 1.0, x1 = 1.0, x2 = 1.0;
-        if (PART != 3) load_vec3(x + t.y, x0, x1, x2);
-        a0 += v[0] * x0 + v[3] * x1 + v[6] * x2;
-        a1 += v[1] * x0 + v[4] * x1 + v[7] * x2;
-        a2 += v[2] * x0 + v[5] * x1 + v[8] * x2;
-      }
-#pragma unroll
-    for (int off = SW / 2; off > 0; off >>= 1) {
-      a0 += __shfl_xor_sync(mask, a0, off, SW);
-      a1 += __shfl_xor_sync(mask, a1, off, SW);
-      a2 += __shfl_xor_sync(mask, a2, off, SW);
-    }
-    if (lane == 0) {
-      y[3 * R] = a0;
-      y[3 * R + 1] = a1;
-      y[3 * R + 2] = a2;
-    }
-  }
-}
-
-template <int SW, int MINB>
-__global__ void __launch_bounds__(kTB, MINB) k_spmv33_u2(SpmvDev S0, SpmvDev S1, int has1, int64_t nb,
-                                                         const double* __restrict__ x, double* __restrict__ y) {
-  const int lane = threadIdx.x % SW;
-  const int64_t sw0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / SW;
-  const int64_t nsw = int64_t(gridDim.x) * blockDim.x / SW;
-  const unsigned mask = ((1u << SW) - 1u) << ((threadIdx.x & 31) & ~(SW - 1));
-  for (int64_t R = sw0; R < nb; R += nsw) {
-    const RowPtrs p0 = load_rowptrs(S0, R);
-    RowPtrs p1{0, 0, 0, 0};
-    if (has1) p1 = load_rowptrs(S1, R);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    acc33_u2<SW>(S0, p0, lane, x, a0, a1, a2);
-    if (has1) acc33_u2<SW>(S1, p1, lane, x, a0, a1, a2);
-#pragma unroll
-    for (int off = SW / 2; off > 0; off >>= 1) {
-      a0 += __shfl_xor_sync(mask, a0, off, SW);
-      a1 += __shfl_xor_sync(mask, a1, off, SW);
-      a2 += __shfl_xor_sync(mask, a2, off, SW);
-    }
-    if (lane == 0) {
-      y[3 * R] = a0;
-      y[3 * R + 1] = a1;
-      y[3 * R + 2] = a2;
-    }
-  }
-}
-
-template <class K>
-static void launch_u2(Context& c, K kern, const double* x, double* y) {
-  int occ = 0;
-  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
-  const bool has1 = c.S[1].n_blocks > 0;
-  SpmvDev d0 = spmv_dev(c.S[0]), d1 = spmv_dev(c.S[has1 ? 1 : 0]);
-  kern<<<std::max(1, occ) * sm_count(), kTB, 0, c.stream>>>(d0, d1, has1 ? 1 : 0, c.NB, x, y);
-  YS_LAUNCH_CHECK();
-}
-
-template <class K>
-static void launch_var(Context& c, K kern, SpmvDev d0, const double* x, double* y) {
-  int occ = 0;
-  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
-  kern<<<std::max(1, occ) * sm_count(), kTB, 0, c.stream>>>(d0, c.NB, x, y);
-  YS_LAUNCH_CHECK();
-}
-
-bool spmv_variant(Context& c, int v, const double* x, double* y) {
-  SpmvDev d0 = spmv_dev(c.S[0]);
-  switch (v) {
-    case 1: launch_var(c, k_spmv33_var<8, 3, 0, false>, d0, x, y); return true;
-    case 2: launch_var(c, k_spmv33_var<8, 4, 0, false>, d0, x, y); return true;
-    case 3: launch_var(c, k_spmv33_var<8, 5, 0, false>, d0, x, y); return true;
-    case 4: launch_var(c, k_spmv33_var<8, 4, 1, false>, d0, x, y); return true;  // own-row blocks only
-    case 5: launch_var(c, k_spmv33_var<8, 4, 2, false>, d0, x, y); return true;  // transposed only
-    case 6: launch_var(c, k_spmv33_var<8, 4, 3, false>, d0, x, y); return true;  // no x gathers
-    case 7: launch_var(c, k_spmv33_var<8, 4, 0, true>, d0, x, y); return true;   // + row-pointer prefetch
-    case 8: launch_var(c, k_spmv33_var<4, 4, 0, false>, d0, x, y); return true;  // 4 lanes per row
-    case 9: launch_var(c, k_spmv33_var<4, 4, 0, true>, d0, x, y); return true;
-    case 10: launch_var(c, k_spmv33_var<16, 4, 0, false>, d0, x, y); return true;
-    case 11: launch_var(c, k_spmv33_var<4, 5, 0, true>, d0, x, y); return true;
-    case 12: launch_var(c, k_spmv33_var<2, 4, 0, true>, d0, x, y); return true;
-    // static + dynamic, two entries per lane per trip (13: one entry per trip, the pre-u2 kernel)
-    case 13: launch_u2(c, k_spmv33_u2<4, 4>, x, y); return true;
-    case 14: launch_u2(c, k_spmv33_u2<4, 3>, x, y); return true;
-    case 15: launch_u2(c, k_spmv33_u2<8, 3>, x, y); return true;
-    case 16: launch_u2(c, k_spmv33_u2<2, 3>, x, y); return true;
-    case 17: launch_u2(c, k_spmv33_u2<4, 2>, x, y); return true;
-  }
-  return false;
-}
 
 // Generic shapes: one warp per block row of size RC (launched per block-size
 // class), lanes over the row's entries, fixed xor-butterfly reduction.
@@ -1134,38 +1009,6 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
 // 3.1 us, counter barrier 2.2 us, + reduction ~1.1 us.  Also measured and
 // dropped: 32 striped counters 3.5 us, relaxed polling 2.3 us, 256 ns backoff
 // 2.6 us, master release through per-CTA flag lines 4.3 us.
-__global__ void __launch_bounds__(kTB, kSpmvMinB) k_barrier_probe(GridBar* gb, int n, int with_reduce, double* part,
-                                                                  double* out) {
-  double acc = 0.0;
-  for (int k = 0; k < n; ++k) {
-    if (with_reduce & 1) {
-      if (threadIdx.x == 0) part[blockIdx.x] = double(k + blockIdx.x);
-    }
-    if (with_reduce & 2) grid_sync_counter(&gb->arrivals, (unsigned long long)gridDim.x * (k + 1));
-    else grid_sync(gb);
-    if (with_reduce & 1) {
-      double t[1];
-      reduce_partials_all<1>(part, gridDim.x, t);
-      acc += t[0];
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = acc;
-}
-
-void barrier_probe(Context& c, int n, int with_reduce) {
-  void* kern = reinterpret_cast<void*>(k_barrier_probe);
-  int occ = 0;
-  YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
-  int gsz = std::max(1, occ) * sm_count();
-  c.gridbar.resize(sizeof(GridBar));
-  YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), c.stream));
-  c.partials.resize(std::max<size_t>(c.partials.n, size_t(gsz + 1)));
-  GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
-  double* part = c.partials.p;
-  double* out = c.partials.p + gsz;
-  void* args[] = {&gbp, &n, &with_reduce, &part, &out};
-  YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, c.stream));
-}
 
 void ctx_apply_hessian_dev(Context& c, const double* x, double* y) {
   spmv_launch(c, c.S[0], &c.S[1], x, y, true, nullptr, nullptr, std::max(1, sm_count() * 8));
@@ -1257,13 +1100,13 @@ void drop_pcg_graph(Context& c) {
 
 int pcg_grid(Context& c) { return std::max(1, sm_count() * 8); }
 
-// The layout half of the uniform-3x3 solve's copy of H (the symmetric band
-// copy, ys_sym.cu), when the next ctx_pcg will take that path: built right
-// after the dynamic rebuild, while the static evaluation runs on the side streams.
+// The layout half of the uniform-3x3 solve's sliced-ELL copy (sell_prepare):
+// built right after the dynamic rebuild, while the static evaluation still runs
+// on the side streams.
 void pcg_prepare(Context& c) {
   const bool has1 = c.S[1].n_blocks > 0;
   const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
-  if (fast) sym_prepare(c);
+  if (fast) sell_prepare(c, 4);
 }
 
 void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, double* x_dev, ys_step_stats* stats) {
@@ -1288,11 +1131,10 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
                                   c.pcg.p, c.partials.p, c.hist.p);
   YS_LAUNCH_CHECK();
 
-  // Uniform 3x3 systems: one persistent cooperative kernel runs the whole solve,
-  // over the symmetric band copy (ys_sym.cu); when its layout does not fit
-  // the shared memory, over the sliced-ELL full copy, and when that plan does
-  // not fit either, the row gather from upper storage.  The path taken is
-  // reported (ys_stage_times, "pcg_path").
+  // Uniform 3x3 systems: one persistent cooperative kernel runs the whole solve
+  // over the sliced-ELL full copy; when its per-warp plan does not fit the
+  // shared memory (systems several times C5 per GPU), over the row gather from
+  // upper storage.  The path taken is reported (ys_stage_times counts[2]).
   {
     const bool has1 = c.S[1].n_blocks > 0;
     const bool fast = c.uniform3 && c.S[0].all33 && (!has1 || c.S[1].all33);
@@ -1301,9 +1143,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       const double* minv = c.minv.p;
       double *xp = c.DX.p, *rp = c.r.p, *zp = c.z.p, *pp = c.p.p, *hpp = c.hp.p, *hist = c.hist.p;
       PcgState* stp = c.pcg.p;
-      static const bool sym_off = getenv("YS_EXPERIMENT_SELL") != nullptr;  // temporary A/B switch
-      bool launched = !sym_off && sym_pcg(c, stats);
-      if (launched) c.pcg_path = 1;
+      bool launched = false;
       c.gridbar.resize(sizeof(GridBar));
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
       if (!launched) {
@@ -1336,7 +1176,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
           void* args[] = {&A, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
           YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, smem, s));
           launched = true;
-          c.pcg_path = 2;
+          c.pcg_path = 1;
         }
       }
       if (!launched) {
@@ -1354,7 +1194,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         double* part = c.partials.p;
         void* args[] = {&d0, &d1, &sl, &h1, &nb, &minv, &xp, &rp, &zp, &pp, &hpp, &stp, &part, &hist, &gbp};
         YS_CUDA(cudaLaunchCooperativeKernel(kern, dim3(gsz), dim3(kTB), args, 0, s));
-        c.pcg_path = 3;
+        c.pcg_path = 2;
       }
       PcgState fin{};
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
@@ -1379,8 +1219,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
   }
   // Mixed block sizes: one persistent cooperative kernel (YS_PCG_GEN=graph keeps
   // the graph-looped kernels).
-  static const bool gen_graph = getenv("YS_PCG_GEN") && std::string(getenv("YS_PCG_GEN")) == "graph";
-  if (!gen_graph && c.rc_classes.size() <= 8) {
+  if (c.rc_classes.size() <= 8) {
     GenClasses cls{};
     cls.n = int(c.rc_classes.size());
     for (int k = 0; k < cls.n; ++k) {
@@ -1449,39 +1288,24 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
                                P(c.partials.p), P(c.hist.p),
                                uint64_t(s1.n_blocks > 0) | (uint64_t(s0.all33) << 1) | (uint64_t(s1.all33) << 2),
                                uint64_t(grid), uint64_t(c.s)};
-  // YS_PCG_GRAPH: "cond" (default: device-side while loop), "chunk" (graph of 8
-  // iterations, host checks the status per chunk), "none" (plain launches —
-  // for ncu, which cannot profile kernels inside conditional graphs).
-  static const int mode = [] {
-    const char* e = getenv("YS_PCG_GRAPH");
-    if (!e) return 0;
-    return std::string(e) == "chunk" ? 1 : std::string(e) == "none" ? 2 : 0;
-  }();
   PcgState fin{};
-  if (mode == 2) {
+  // a device-side WHILE loop (conditional graph node); when the driver cannot
+  // build one, graphs of 8 iterations with a status read per graph
+  if (!c.pcg_exec || c.pcg_key != key) {
+    drop_pcg_graph(c);
+    if (!build_conditional_graph(c, grid)) build_chunk_graph(c, grid, 8);
+    c.pcg_key = key;
+  }
+  if (c.pcg_cond) {
+    YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
+    YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+  } else {
     for (;;) {
       YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       YS_CUDA(cudaStreamSynchronize(s));
       if (fin.status) break;
-      for (int k = 0; k < 8; ++k) launch_iteration(c, grid, cudaGraphConditionalHandle{}, false);
-    }
-  } else {
-    if (!c.pcg_exec || c.pcg_key != key) {
-      drop_pcg_graph(c);
-      if (mode == 1 || !build_conditional_graph(c, grid)) build_chunk_graph(c, grid, 8);
-      c.pcg_key = key;
-    }
-    if (c.pcg_cond) {
       YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
-      YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-      YS_CUDA(cudaStreamSynchronize(s));
-    } else {
-      for (;;) {
-        YS_CUDA(cudaMemcpyAsync(&fin, c.pcg.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-        YS_CUDA(cudaStreamSynchronize(s));
-        if (fin.status) break;
-        YS_CUDA(cudaGraphLaunch(c.pcg_exec, s));
-      }
     }
   }
   c.launches += 2 + 3 * fin.it;

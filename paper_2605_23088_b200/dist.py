@@ -15,8 +15,8 @@ import numpy as np
 from . import _lib
 
 
-def unique_id(backend: str = "gpu") -> bytes:
-    lib = _lib.gpu_library() if backend == "gpu" else _lib.oracle_library()
+def unique_id(lib: _lib.Library | None = None) -> bytes:
+    lib = lib or _lib.gpu_library()
     if not lib.has("dist_unique_id"):
         raise _lib.DeclError(f"{lib.path.name} has no NCCL transport")
     buf = C.create_string_buffer(128)
@@ -30,7 +30,7 @@ def init_nccl(eng, group=None):
     import torch
     import torch.distributed as dist
     rank, n = dist.get_rank(group), dist.get_world_size(group)
-    uid = unique_id(eng.backend) if rank == 0 else bytes(128)
+    uid = unique_id(eng.lib) if rank == 0 else bytes(128)
     t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).clone()
     if dist.get_backend(group) == "nccl":
         t = t.cuda()

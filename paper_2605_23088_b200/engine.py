@@ -1,8 +1,8 @@
 """Python mirror of relsim::Engine over the C-ABI (engine.hpp:27-80).
 
-`Engine` drives one context of a C-ABI implementation: the B200 library by
-default, or — for parity tests only — the CPU oracle / the reference build,
-which export the same functions.  Method names, argument meaning and raised
+`Engine` drives one context of the B200 library (tests may inject another
+implementation of the same C-ABI — see oracle/__init__.py; the product never
+does).  Method names, argument meaning and raised
 exception classes follow the reference.
 """
 from __future__ import annotations
@@ -145,16 +145,8 @@ def merged_coordinate_text(eng: "Engine") -> str:
 
 
 class Engine:
-    def __init__(self, backend: str = "gpu", device: int = 0):
-        if backend == "gpu":
-            self.lib = _lib.gpu_library()
-        elif backend == "oracle":
-            self.lib = _lib.oracle_library()
-        elif backend == "reference":
-            self.lib = _lib.reference_library()
-        else:
-            raise ValueError(backend)
-        self.backend = backend
+    def __init__(self, device: int = 0, library: _lib.Library | None = None):
+        self.lib = library if library is not None else _lib.gpu_library()
         self.f = self.lib.fns
         h = C.c_void_p()
         st = self.f["create"](C.byref(h), device)
@@ -497,24 +489,16 @@ class Engine:
         self._c(self.f["stream"](self.ctx, C.byref(h)))
         return h.value or 0
 
+    def set_option(self, name: str, value: int):
+        """Execution options that do not change results (ys_set_option)."""
+        self._c(self.f["set_option"](self.ctx, name.encode(), int(value)))
+
     def pcg_path(self) -> str:
         """Kernel path of the last uniform-3x3 solve."""
         ms = np.zeros(16)
         cnt = np.zeros(3, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
-        return {1: "symmetric band copy", 2: "sliced-ELL copy", 3: "row gather"}.get(int(cnt[2]), "general")
-
-    def pcg_layout_info(self, per_cta: bool = False):
-        """Sizes of the last symmetric band copy (and per-CTA clocks of its solve)."""
-        info = np.zeros(12, dtype=np.int64)
-        cta = np.zeros(8 * 1024, dtype=np.int64)
-        self._c(self.f["pcg_layout_info"](self.ctx, _ip64(info), _ip64(cta)))
-        keys = ["ctas", "tiles", "max_rows", "window", "stages", "stage_bytes", "max_blocks_per_tile", "near",
-                "far", "spill_slots", "smem", "usable"]
-        d = dict(zip(keys, info.tolist()))
-        if per_cta:
-            d["cta"] = cta[:8 * d["ctas"]].reshape(-1, 8)
-        return d
+        return {1: "sliced-ELL copy", 2: "row gather"}.get(int(cnt[2]), "general")
 
     def time_kernel(self, which: int, reps: int = 20):
         ms, b = C.c_double(), C.c_double()

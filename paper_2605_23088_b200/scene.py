@@ -1,11 +1,11 @@
 """Scene construction and the Newton driver, mirroring relsim's Simulation.
 
-`Simulation(config, backend)` builds the same targets, point domains, energies
-and contact union as Simulation::build_from_config (sim.cpp:212-451), in the
-same registration order, then drives frames exactly like Simulation::step /
+`Simulation(config)` builds the same targets, point domains, energies and
+contact union as Simulation::build_from_config (sim.cpp:212-451), in the same
+registration order, then drives frames exactly like Simulation::step /
 newton_solve (sim.cpp:488-581).  The engine underneath is the C-ABI
-(`Engine`), i.e. the B200 library unless a test passes backend="oracle" /
-"reference".
+(`Engine`) of the B200 library (tests inject the oracle's library through
+`library=`).
 """
 from __future__ import annotations
 
@@ -173,9 +173,9 @@ def _vec3(j, fallback):
 
 
 class Simulation:
-    def __init__(self, config: SimConfig, backend: str = "gpu", device: int = 0, refresh_pairs: bool = True):
+    def __init__(self, config: SimConfig, device: int = 0, refresh_pairs: bool = True, library=None):
         self.config = config
-        self.eng = Engine(backend, device)
+        self.eng = Engine(device, library)
         self.bodies: list[Body] = []
         self.dt2 = config.dt * config.dt
         self.contact_pairset = -1

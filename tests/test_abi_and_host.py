@@ -11,7 +11,9 @@ import numpy as np
 import pytest
 
 from paper_2605_23088_b200 import ValidationError, configs
-from paper_2605_23088_b200._lib import LIB_PATH, ROOT, gpu_library, oracle_library
+import oracle
+from backends import engine
+from paper_2605_23088_b200._lib import LIB_PATH, ROOT, gpu_library
 from paper_2605_23088_b200.scene import SimConfig, hinges, make_grid_cloth, make_tet_block
 
 HEADER = ROOT / "include" / "yasps_b200.h"
@@ -39,7 +41,7 @@ def test_b200_library_exports_every_declared_symbol():
 
 
 def test_oracle_exports_the_same_abi():
-    lib = oracle_library()
+    lib = oracle.library()
     dll = lib.dll
     # device instrumentation and the NCCL transport have no CPU counterpart
     optional = {"ys_set_profiling", "ys_stage_times", "ys_device_bytes", "ys_time_kernel", "ys_dist_unique_id",
@@ -61,7 +63,7 @@ def test_no_device_means_loud_failure():
             pytest.skip("a device is present")
     from paper_2605_23088_b200 import CudaError, Engine
     with pytest.raises(CudaError):
-        Engine("gpu")
+        engine("gpu")
 
 
 def test_tet_block_sizes_match_survey():

@@ -20,8 +20,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _scene(backend):
     from paper_2605_23088_b200 import configs
-    from paper_2605_23088_b200.scene import SimConfig, Simulation
-    sim = Simulation(SimConfig.from_dict(configs.c1()), backend=backend)
+    from paper_2605_23088_b200.scene import SimConfig
+    from backends import simulation
+    sim = simulation(SimConfig.from_dict(configs.c1()), backend)
     configs.jitter_targets(sim, 0.0025)
     sim.begin_frame()
     sim.refresh_dynamic_pairs()

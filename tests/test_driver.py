@@ -11,6 +11,7 @@ import pytest
 
 from paper_2605_23088_b200 import BlockSystem
 from paper_2605_23088_b200.scene import SimConfig, Simulation
+from backends import simulation  # noqa: E402
 
 BACKENDS = ["oracle", pytest.param("gpu", marks=pytest.mark.gpu)]
 
@@ -46,7 +47,7 @@ BLOCK_ON_CLOTH = {  # scenes/block_on_cloth.json
 @pytest.mark.parametrize("backend", BACKENDS)
 def test_proximity_refresh_kat(backend):
     # test_sim.cpp:102-137
-    sim = Simulation(SimConfig.from_dict(TWO_POINT), backend=backend)
+    sim = simulation(SimConfig.from_dict(TWO_POINT), backend)
     a, b = sim.bodies
     sim.eng.set_target_values(a.targets[0], [0.0, 0.0, 0.0, 0.05, 0.0, 0.0])
     sim.eng.set_target_values(b.targets[0], [0.04, 0.0, 0.0, 0.09, 0.05, 0.0])
@@ -64,7 +65,7 @@ def test_free_fall_one_step(backend):
     # test_sim.cpp:139-157: convex quadratic -> exact after one Newton step
     cfg = {"name": "quad", "dt": 0.01, "frames": 1, "gravity": [0, -9.8, 0],
            "bodies": [{"name": "a", "kind": "free_points", "mass": 2.0, "points": [[0, 0, 0], [1, 0, 0], [0, 1, 0]]}]}
-    sim = Simulation(SimConfig.from_dict(cfg), backend=backend)
+    sim = simulation(SimConfig.from_dict(cfg), backend)
     rep = sim.step()
     assert rep.converged and rep.iterations <= 2 and rep.energy_nonincreasing
     sim.eng.assemble(True, False)
@@ -76,7 +77,7 @@ def test_free_fall_one_step(backend):
 @pytest.mark.parametrize("backend", BACKENDS)
 def test_energy_nonincreasing_stiff_contact(backend):
     # test_sim.cpp:159-169 on scenes/contact_pair.json (free + affine bodies)
-    sim = Simulation(SimConfig.from_dict(CONTACT_PAIR), backend=backend)
+    sim = simulation(SimConfig.from_dict(CONTACT_PAIR), backend)
     for _ in range(20):
         rep = sim.step()
         assert rep.energy_nonincreasing and math.isfinite(rep.energy)
@@ -87,7 +88,7 @@ def test_deterministic_rerun(backend):
     # test_sim.cpp:171-195: byte-identical reruns
     runs = []
     for _ in range(2):
-        sim = Simulation(SimConfig.from_dict(CONTACT_PAIR), backend=backend)
+        sim = simulation(SimConfig.from_dict(CONTACT_PAIR), backend)
         for _ in range(8):
             sim.step()
         runs.append(np.concatenate([p.ravel() for p in sim.positions()]))
@@ -98,7 +99,7 @@ def test_deterministic_rerun(backend):
 def test_block_jacobi_beats_identity_on_block_on_cloth(backend):
     # test_acceptance.cpp:456-473: 25 frames to a contact-rich state, then
     # PCG with block Jacobi takes strictly fewer iterations than identity
-    sim = Simulation(SimConfig.from_dict(BLOCK_ON_CLOTH), backend=backend)
+    sim = simulation(SimConfig.from_dict(BLOCK_ON_CLOTH), backend)
     for _ in range(25):
         sim.step()
     eng = sim.eng

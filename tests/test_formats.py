@@ -12,6 +12,7 @@ import pytest
 
 from paper_2605_23088_b200.engine import HessianStructure, matrix_market_text, merged_coordinate_text
 from paper_2605_23088_b200.scene import SimConfig, Simulation
+from backends import simulation  # noqa: E402
 
 from test_driver import BLOCK_ON_CLOTH, CONTACT_PAIR
 
@@ -72,7 +73,7 @@ def test_merged_text_sums_in_map_order():
 
 def test_run_writes_trajectory_and_stats(tmp_path):
     cfg = dict(CONTACT_PAIR, frames=3, output_dir=str(tmp_path / "out"))
-    sim = Simulation(SimConfig.from_dict(cfg), backend="oracle")
+    sim = simulation(SimConfig.from_dict(cfg), "oracle")
     log = io.StringIO()
     sim.run(log)
     traj = (tmp_path / "out" / "trajectory.txt").read_text().splitlines()
@@ -97,7 +98,7 @@ def test_run_writes_trajectory_and_stats(tmp_path):
 def test_export_matrix_gpu_matches_oracle():
     texts = []
     for backend in ("oracle", "gpu"):
-        sim = Simulation(SimConfig.from_dict(BLOCK_ON_CLOTH), backend=backend)
+        sim = simulation(SimConfig.from_dict(BLOCK_ON_CLOTH), backend)
         texts.append(sim.export_matrix(frame=5).splitlines())
     a, b = texts
     assert a[:3] == b[:3]

@@ -13,6 +13,7 @@ from paper_2605_23088_b200 import NumericalError, ValidationError
 from paper_2605_23088_b200.engine import (YS_POINTS_AFFINE, YS_POINTS_FIXED, YS_POINTS_FREE, YS_PROJECT_FULL,
                                           YS_PROJECT_REDUCED, BlockSystem, Engine)
 from fixtures import ContactScene, random_system, rel, tet_scene
+from backends import engine, simulation  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-9
@@ -21,7 +22,7 @@ TOL = 1e-9
 def both(build):
     out = []
     for backend in ("gpu", "oracle"):
-        eng = Engine(backend)
+        eng = engine(backend)
         handles = build(eng)
         eng.finalize()
         out.append((eng, handles))
@@ -160,7 +161,7 @@ def test_minimize_step_matches_oracle():
     from paper_2605_23088_b200.scene import SimConfig, Simulation
 
     cfg = SimConfig.from_dict(configs.c3())
-    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    sims = [simulation(cfg, b) for b in ("gpu", "oracle")]
     for s in sims:
         configs.jitter_targets(s, 0.002)
         s.begin_frame()
@@ -184,7 +185,7 @@ def test_minimize_step_uniform_scene_matches_oracle():
     from paper_2605_23088_b200.scene import SimConfig, Simulation
 
     cfg = SimConfig.from_dict(configs.c2())
-    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    sims = [simulation(cfg, b) for b in ("gpu", "oracle")]
     for s in sims:
         configs.jitter_targets(s, 0.001)
         s.begin_frame()
@@ -207,7 +208,7 @@ def test_block_system_spmv_and_pcg():
         s, coords, vals = random_system(nb, bs, 0.3, seed)
         systems = []
         for backend in ("gpu", "oracle"):
-            eng = Engine(backend)
+            eng = engine(backend)
             bsys = BlockSystem(eng, s, np.asarray(coords).reshape(-1))
             v = np.zeros(bsys.n_values)
             for (r, c), b in vals.items():
@@ -232,7 +233,7 @@ def test_numerical_errors_match_reference_wording():
     # singular / non-finite diagonal block names the DoF range (test_solver.cpp:176-194)
     s, coords, vals = random_system(2, 3, 0.0, 5)
     for backend in ("gpu", "oracle"):
-        eng = Engine(backend)
+        eng = engine(backend)
         bsys = BlockSystem(eng, s, np.asarray(coords).reshape(-1))
         v = np.zeros(bsys.n_values)
         v[0:9] = np.eye(3).ravel()
@@ -253,7 +254,7 @@ def test_refresh_pairs_bit_exact():
     from paper_2605_23088_b200.scene import SimConfig, Simulation
 
     cfg = SimConfig.from_dict(configs.c3())
-    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    sims = [simulation(cfg, b) for b in ("gpu", "oracle")]
     for s in sims:
         configs.jitter_targets(s, 0.004, seed=99)
     n = [s.refresh_dynamic_pairs() for s in sims]
@@ -269,7 +270,7 @@ def test_newton_frames_positions():
     from paper_2605_23088_b200.scene import SimConfig, Simulation
 
     cfg = SimConfig.from_dict(configs.c1())
-    sims = [Simulation(cfg, backend=b) for b in ("gpu", "oracle")]
+    sims = [simulation(cfg, b) for b in ("gpu", "oracle")]
     for frame in range(3):
         reps = [s.step() for s in sims]
         assert reps[0].iterations == reps[1].iterations
@@ -322,29 +323,24 @@ def test_contact_candidates_grid_bit_exact(dhat):
         assert ng > 0
 
 
-def test_overlap_and_sequential_steps_are_bitwise_equal():
-    """The static energies' evaluation on the second stream (overlapping the
-    dynamic rebuild) must give exactly the sequential step (YS_OVERLAP=0)."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_overlap_and_sequential_steps_are_bitwise_equal(name):
+    """The static energies' evaluation on side streams (overlapping the dynamic
+    rebuild, the default) must give exactly the sequential step
+    (ys_set_option("overlap", 0))."""
+    import hashlib
 
-    code = (
-        "import hashlib, numpy as np\n"
-        "from paper_2605_23088_b200 import configs\n"
-        "from paper_2605_23088_b200.scene import SimConfig, Simulation\n"
-        "cfg = SimConfig.from_dict(configs.c3())\n"
-        "sim = Simulation(cfg, backend='gpu')\n"
-        "configs.jitter_targets(sim, 0.002)\n"
-        "sim.begin_frame(); sim.refresh_dynamic_pairs()\n"
-        "st = sim.eng.minimize_step(1e-4)\n"
-        "print(hashlib.sha256(np.ascontiguousarray(st.dx).tobytes()).hexdigest(), st.pcg_iterations)\n"
-    )
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+
     outs = []
-    for ov in ("1", "0"):
-        env = dict(os.environ, YS_OVERLAP=ov, PYTHONPATH=root)
-        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(r.stdout.strip().splitlines()[-1])
+    for ov in (1, 0):
+        cfg = SimConfig.from_dict(configs.CONFIGS[name]())
+        sim = Simulation(cfg)
+        sim.eng.set_option("overlap", ov)
+        configs.jitter_targets(sim, 0.002 if name == "c3" else 0.001)
+        sim.begin_frame()
+        sim.refresh_dynamic_pairs()
+        st = sim.eng.minimize_step(1e-4)
+        outs.append((hashlib.sha256(np.ascontiguousarray(st.dx).tobytes()).hexdigest(), st.pcg_iterations))
     assert outs[0] == outs[1], outs

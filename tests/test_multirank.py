@@ -19,8 +19,9 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2605_23088_b200 import configs
-    from paper_2605_23088_b200.scene import SimConfig, Simulation
-    sim = Simulation(SimConfig.from_dict(configs.c1()), backend="oracle")
+    from paper_2605_23088_b200.scene import SimConfig
+    from backends import simulation
+    sim = simulation(SimConfig.from_dict(configs.c1()), "oracle")
     configs.jitter_targets(sim, 0.0025)
     sim.begin_frame()
     sim.refresh_dynamic_pairs()

@@ -13,6 +13,7 @@ from paper_2605_23088_b200 import DeclError, NumericalError, ValidationError
 from paper_2605_23088_b200.engine import (YS_POINTS_FIXED, YS_POINTS_FREE, YS_PROJECT_REDUCED, BlockSystem,
                                           Engine)
 from fixtures import ContactScene, random_system, rel, tet_scene
+from backends import engine  # noqa: E402
 
 
 BACKENDS = ["oracle", pytest.param("gpu", marks=pytest.mark.gpu)]
@@ -22,7 +23,7 @@ BACKENDS = ["oracle", pytest.param("gpu", marks=pytest.mark.gpu)]
 def mk(request):
     """Engine factory for the backend under test: the oracle on CPU, the B200
     library on the GPU leg (the same known answers pin both)."""
-    return lambda: Engine(request.param)
+    return lambda: engine(request.param)
 
 
 # ---------------------------------------------------------------- layout / slots (test_index.cpp)

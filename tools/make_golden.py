@@ -14,14 +14,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2605_23088_b200 import configs  # noqa: E402
-from paper_2605_23088_b200.scene import SimConfig, Simulation  # noqa: E402
+from paper_2605_23088_b200.scene import SimConfig  # noqa: E402
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from backends import simulation  # noqa: E402
 
 JITTER = {"c1": 0.0025, "c2": 0.001, "c3": 0.002}
 
 
 def step_record(name: str, backend: str):
     cfg = SimConfig.from_dict(configs.CONFIGS[name]())
-    sim = Simulation(cfg, backend=backend)
+    sim = simulation(cfg, backend)
     configs.jitter_targets(sim, JITTER[name])
     sim.begin_frame()
     sim.refresh_dynamic_pairs()

@@ -9,5 +9,5 @@ sim = prepare(name, True, "gpu")
 eng = sim.eng
 st = eng.minimize_step(sim.config.pcg_tol, -1, want_dx=False)
 print("pcg iterations", st.pcg_iterations, flush=True)
-for which in (42, 1, 2):  # SELL SpMV (4 lanes / row), assembly, eval
+for which in (3, 1, 2):  # SELL SpMV (4 lanes / row), assembly, eval
     print(which, eng.time_kernel(which, 3), flush=True)
