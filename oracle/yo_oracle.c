@@ -22,9 +22,13 @@
  *   - spmv_add (solver.cpp:10-82, serial), BlockJacobiPreconditioner
  *     (93-146), pcg (151-200) verbatim, Engine::minimize_step (engine.cpp:75-101);
  *   - refresh_dynamic_pairs (sim.cpp:456-484) all-pairs loop.
- * Parity pinning: tests/test_oracle.py checks it against the reference's own
- * known-answer tests and against the reference itself built here
- * (oracle/_ref, see oracle/Makefile).
+ * Parity pinning: the reference itself is built here from its unmodified
+ * sources against eigen-lite (oracle/ref_build.sh -> oracle/_ref: relsim, its
+ * ten doctest suites — all passing — and oracle/ref_driver.cpp).  The goldens
+ * of tests/golden are the reference's own step records; tests/test_golden.py
+ * and tests/test_reference.py check this restatement against them (bit-exact
+ * structure and pairs, equal PCG iteration counts, values <= 1e-9), and
+ * tests/test_oracle.py against the reference's known-answer tests.
  */
 #include <math.h>
 #include <pthread.h>
