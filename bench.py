@@ -147,78 +147,122 @@ def traffic_from_profiles(scene: str, key: str):
         return None
 
 
-def cpu_sample(name: str, via_f: bool, gpu_pcg_iterations: int, budget_s: float = 20.0):
-    """Bounded CPU sample of the same workload on the host through the oracle
-    port (the reference's algorithm restated in C; the reference itself cannot
-    be built here): a single block of the scene (C5: one of the 8
-    soft blocks) is assembled once, and the PCG's per-iteration cost is the
-    difference of two solves capped at 2 and 42 iterations; both are scaled to
-    the full scene and the GPU's PCG iteration count.  Like the reference's
-    parallel_for, the oracle evaluates instances on all host threads
-    (YO_THREADS caps them) and scatters / iterates serially."""
+def oracle_state(name: str, via_f: bool, pairs=None):
+    """The bench's prepared state on the oracle port (the reference's algorithm
+    restated in C, pinned to the reference itself: tests/test_golden.py,
+    tests/test_reference.py): the same config, jitter and begin_frame; the
+    contact pairs from the reference's all-pairs loop, or — for the GPU arm's
+    bounded sample — the GPU's list, which is bit-identical
+    (tests/test_gpu_large.py) and spares the O(n^2) refresh."""
     from paper_2605_23088_b200 import configs
     from paper_2605_23088_b200.scene import SimConfig
-    backend, kind = "oracle", "port"
-    full = scene_config(name, via_f)
-    sub = dict(full)
-    soft = [b for b in full["bodies"] if not b.get("fixed")]
-    sub["bodies"] = [soft[0]] + [b for b in full["bodies"] if b.get("fixed")]
-    sub["contact"] = dict(full["contact"], bodies=[soft[0]["name"]] + [b["name"] for b in full["bodies"] if b.get("fixed")])
-    cfg = SimConfig.from_dict(sub)
-    sim = simulation(cfg, backend, refresh_pairs=False)
+    cfg = SimConfig.from_dict(scene_config(name, via_f))
+    sim = simulation(cfg, "oracle", refresh_pairs=False)
     configs.jitter_targets(sim, jitter_amplitude(name))
     sim.begin_frame()
-    sim.refresh_dynamic_pairs()
+    if sim.contact_pairset >= 0:
+        if pairs is None:
+            sim.refresh_dynamic_pairs()
+        else:
+            sim.eng.set_pairs(sim.contact_pairset, pairs)
+    return sim
+
+
+def cpu_threads() -> int:
+    """All host threads, as the reference configured with "threads" = nproc:
+    instance evaluation (parallel_for, assembly.cpp:334-336) and the sharded
+    spmv_add (solver.cpp:63-81); the scatter and the PCG vector updates stay
+    serial, as in the reference."""
+    n = int(os.environ.get("YO_THREADS") or os.cpu_count() or 1)
+    os.environ["YO_THREADS"] = str(n)
+    os.environ["YO_SPMV_THREADS"] = str(n)
+    return n
+
+
+def cpu_step(sim):
+    """One Newton iteration of the oracle, timed on the host (perf_counter)."""
     eng = sim.eng
-    threads = int(os.environ.get("YO_THREADS") or os.cpu_count() or 1)
-    os.environ["YO_SPMV_THREADS"] = str(threads)  # the reference's threaded spmv_add (solver.cpp:63-81)
-    eng.refresh_dynamic()
+    eng.bump_dynamic_epoch()
     t0 = time.perf_counter()
-    eng.assemble(True, True)
-    t_asm = time.perf_counter() - t0
-    k1, k2 = 2, 42
-    t0 = time.perf_counter()
-    eng.minimize_step(1e-300, k1, want_dx=False)
-    t_a = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    eng.minimize_step(1e-300, k2, want_dx=False)
-    t_b = time.perf_counter() - t0
-    t_pcg_it = max(t_b - t_a, 0.0) / (k2 - k1)
-    s_sub = eng.s
-    scale = len(soft)
-    ms = 1e3 * (t_asm * scale + t_pcg_it * scale * gpu_pcg_iterations)
-    return {"value": ms, "unit": "ms", "cores": threads, "kind": kind,
-            "sample": (f"{name} single soft body ({s_sub} DoFs, 1/{scale} of the scene): one assembly "
-                       f"({t_asm:.2f}s, instance evaluation on {threads} threads) + PCG iterations (SpMV sharded over {threads} threads, "
-                       f"{t_pcg_it*1e3:.2f} ms each, from solves capped at {k1} and {k2}), scaled x{scale} and to "
-                       f"the GPU's {gpu_pcg_iterations} PCG iterations; oracle port library")}
+    st = eng.minimize_step(sim.config.pcg_tol, -1, want_dx=False)
+    return 1e3 * (time.perf_counter() - t0), st
+
+
+def cpu_sample(name: str, via_f: bool, pairs):
+    """Bounded CPU sample for the GPU arm: ONE full-scene Newton iteration of the
+    same workload on the oracle port, on all host threads (~10-20 s at C5)."""
+    threads = cpu_threads()
+    sim = oracle_state(name, via_f, pairs)
+    ms, st = cpu_step(sim)
+    return {"value": ms, "unit": "ms", "cores": threads, "kind": "port",
+            "sample": (f"{name}: one full Newton iteration (minimize_step: dynamic rebuild, instance evaluation on "
+                       f"{threads} threads, assembly, block-Jacobi, PCG with {threads}-shard spmv_add: "
+                       f"{st.pcg_iterations} iterations) of the whole scene on the oracle port — the reference's "
+                       f"algorithm restated in C, pinned to the reference built from its sources")}
 
 
 def run_reference(args):
+    """The reference arm: full-scene Newton iterations of the reference's
+    algorithm on the host cores (the oracle port; the reference itself, built
+    here against eigen-lite, is validated against it but its interpreted plans
+    make a C5 step take tens of minutes), W untimed + K timed steps of the same
+    workload as the GPU arm, from the same prepared state."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # a step = one bounded CPU sample; iteration counts from the oracle itself
-    from paper_2605_23088_b200.scene import SimConfig  # noqa: F401
-    vals = []
-    pcg_it = int(os.environ.get("YASPS_REF_PCG_ITERS", "417"))
-    for k in range(args.warmup + args.steps):
-        cb = cpu_sample(args.config, bool(args.via_f), pcg_it)
-        if k >= args.warmup:
-            vals.append(cb["value"])
-    v = float(statistics.median(vals))
-    cb["value"] = v
+    threads = cpu_threads()
+    t0 = time.perf_counter()
+    sim = oracle_state(args.config, bool(args.via_f))
+    setup_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        cpu_step(sim)
+    vals, iters = [], []
+    for _ in range(args.steps):
+        ms, st = cpu_step(sim)
+        vals.append(ms)
+        iters.append(st.pcg_iterations)
+    v = float(statistics.mean(vals))
+    cb = {"value": v, "unit": "ms", "cores": threads, "kind": "port",
+          "sample": (f"{args.config}: the full scene, {args.warmup} untimed + {args.steps} timed Newton iterations "
+                     f"(minimize_step) on {threads} host threads; PCG iterations {int(np.median(iters))}; "
+                     f"setup (scene build + the reference's all-pairs contact refresh) {setup_s:.1f} s untimed")}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: one Newton iteration (bounded CPU sample, scaled)",
-                       "scene": args.config},
+            "config": {"workload": workload(args.config), "scene": args.config, "dofs": int(sim.eng.s),
+                       "contact_pairs": int(sim.pair_count()), "pcg_iterations": int(np.median(iters)),
+                       "pcg_iterations_per_step": [int(i) for i in iters], "ms_per_step_min": min(vals),
+                       "ms_per_step_max": max(vals), "nh_via_deformation_gradient": bool(args.via_f),
+                       "parallelism": f"host threads {threads}"},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def workload(name: str) -> str:
+    return (f"{name}: one Newton iteration (dynamic rebuild + eval + assembly + block-Jacobi + PCG to pcg_tol) "
+            f"from a jittered rest state")
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch itself as N ranks (one
+    process per GPU) through torch.distributed.run; the driver's own torchrun
+    launch sets WORLD_SIZE and skips this."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world_env:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -325,7 +369,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_sample(args.config, bool(args.via_f), int(np.median(iters)))
+            cpu = cpu_sample(args.config, bool(args.via_f), _read_pairs(sim) if sim.contact_pairset >= 0 else None)
         except Exception as exc:  # reported, not fatal
             cpu = {"value": None, "unit": "ms", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -337,15 +381,14 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: one Newton iteration (dynamic rebuild + eval + assembly + "
-                               f"block-Jacobi + PCG to pcg_tol) from a jittered rest state",
+        "config": {"workload": workload(args.config),
                    "scene": args.config, "tets": stats_tets, "dofs": int(eng.s),
                    "contact_pairs": int(sim.pair_count()), "pcg_iterations": int(np.median(iters)),
                    "nh_via_deformation_gradient": bool(args.via_f),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
                    "parallelism": f"pcg-rows{world} (eval/assembly replicated)" if world > 1 else "single"},
         "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else
-                     "row-partitioned PCG (k_dspmv33 / k_dupdate per rank + NCCL allgather)",
+                     "row-partitioned PCG (k_dspmv_sell / k_dupdate per rank + NCCL allgather)",
                      "bound": "hbm", "achieved": pcg_gbs, "peak": peak, "unit": "GB/s", "frac": pcg_gbs / peak,
                      "traffic": traffic_from_profiles(args.config, "pcg_dram_bytes_per_iteration"),
                      "algorithmic_bytes": pcg_iter_bytes,

@@ -278,8 +278,9 @@ int ys_set_option(ys_context* ctx, const char* name, int64_t value);
  * context stream.  which: 0 = SpMV row gather from upper storage (static +
  * dynamic), 1 = assembly gather + gradient / diagonal / preconditioner rows,
  * 2 = local evaluation of all energies, 3 = the PCG's SpMV through the
- * sliced-ELL copy (uniform 3x3 systems).  avg_ms per launch; bytes =
- * algorithmic bytes per launch. */
+ * sliced-ELL copy (uniform 3x3 systems), 4 = FP64 FMA peak probe (bytes
+ * returns its FLOPs per launch).  avg_ms per launch; bytes = algorithmic bytes
+ * per launch. */
 int ys_time_kernel(ys_context* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);
 
 

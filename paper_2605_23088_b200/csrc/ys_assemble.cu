@@ -470,6 +470,30 @@ __global__ void k_sum_partials(const double* __restrict__ v, int64_t n, double* 
 }
 
 // ---------------------------------------------------------------------------
+// FP64 FMA peak probe (the denominator of the local evaluation's roofline):
+// 8 independent DFMA chains per thread, 8 resident CTAs of 256 per SM.
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = double(threadIdx.x + k) * 1e-9;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t += x[k];
+  if (t == 12345.0) out[0] = t;  // never true: keeps the chains alive
+}
+
+double fp64_probe(Context& c) {
+  const int grid = sm_count() * 8, iters = 4096;
+  c.scratch.resize(std::max<size_t>(c.scratch.n, 16));
+  k_dfma_probe<<<grid, 256, 0, c.stream>>>(c.scratch.p, iters, 0.9999999, 1e-7);
+  YS_LAUNCH_CHECK();
+  return 2.0 * 8.0 * double(iters) * double(grid) * 256.0;  // flops per launch
+}
+
+// ---------------------------------------------------------------------------
 // Assembly gather: unique block u = sum of its sorted contribution run.
 __global__ void k_gather_h(const int64_t* __restrict__ seg, const uint32_t* __restrict__ perm,
                            const double* __restrict__ hc, int64_t u0, int64_t cnt, int rc,

@@ -50,6 +50,7 @@ void spmv_launch(Context& c, Structure& s0, Structure* s1, const double* x, doub
                  PcgState* st, double* part, int grid);
 int pcg_grid(Context& c);
 void ctx_block_rows(Context& c, bool want_h);
+double fp64_probe(Context& c);
 
 
 namespace {
@@ -1220,6 +1221,8 @@ int ys_time_kernel(ys_context* c, int32_t which, int32_t reps, double* avg_ms, d
         ctx_block_rows(*c, true);
       } else if (which == 2) {
         ctx_eval_all(*c, true, true);
+      } else if (which == 4) {
+        alg = fp64_probe(*c);
       } else {
         fail(YS_ERR_VALIDATION, "ys_time_kernel: unknown kernel class");
       }
