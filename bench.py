@@ -320,6 +320,9 @@ def main():
     spmv_ms, spmv_bytes = eng.time_kernel(3, 50)  # the PCG's SpMV: sliced-ELL copy, 4 lanes per row
     asm_ms, asm_bytes = eng.time_kernel(1, 10)
     eval_ms, _ = eng.time_kernel(2, 5)
+    fp64_ms, fp64_flops = eng.time_kernel(4, 5)  # FP64 FMA peak probe (this box, this run)
+    fp64_peak = fp64_flops / (fp64_ms * 1e-3) / 1e12
+    eval_flops = traffic_from_profiles(args.config, "eval_flops_per_step")
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
     asm_gbs = asm_bytes / (asm_ms * 1e-3) / 1e9
     # The dominant kernel is the PCG (one persistent cooperative launch per
@@ -401,6 +404,13 @@ def main():
         "assembly_roofline": {"bound": "hbm", "achieved": asm_gbs, "peak": peak, "unit": "GB/s",
                               "frac": asm_gbs / peak, "algorithmic_bytes": asm_bytes, "avg_ms": asm_ms},
         "eval_ms": eval_ms,
+        "eval_roofline": {"bound": "fp64", "kernel": "k_eval_* (pass A: gradient + H_D + Cholesky test; pass B: 9x9 Jacobi of the indefinite elements; point terms)",
+                          "achieved": (eval_flops / (eval_ms * 1e-3) / 1e12) if eval_flops else None,
+                          "peak": fp64_peak, "unit": "TFLOP/s",
+                          "frac": (eval_flops / (eval_ms * 1e-3) / 1e12 / fp64_peak) if eval_flops else None,
+                          "flops_per_launch": eval_flops, "avg_launch_ms": eval_ms,
+                          "flops_source": "ncu SASS counts 2 DFMA + DADD + DMUL of every k_eval* launch of one step (profiles/ncu_summary.json)",
+                          "peak_source": "measured: k_dfma_probe (8 independent DFMA chains per thread, 8 CTAs of 256 per SM) timed in this run"},
         "stages_ms": {"refresh_dynamic": stages[0], "local_eval": stages[1], "assembly_gather": stages[2],
                       "gradient_diag_precond": stages[3], "pcg": stages[4], "total": stages[6]},
         "gpu_launches": int(launches_per_step * args.steps),

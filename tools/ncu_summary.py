@@ -1,7 +1,8 @@
 """Summarise ncu outputs into profiles/ (tracked):
   launches csv (--metrics gpu__time_duration.sum)  -> per-kernel share table
   full capture (.ncu-rep)                           -> per-kernel metric table + ncu_summary.json
-usage: python tools/ncu_summary.py <tag> <scene> <launches.csv> <prof.ncu-rep> [prof_driver.log]
+  eval FLOP counts csv (--metrics ...dfma/dadd/dmul)  -> eval_flops_per_step in ncu_summary.json
+usage: python tools/ncu_summary.py <tag> <scene> <launches.csv> <prof.ncu-rep> [prof_driver.log] [evalflops.csv]
 (the log's "pcg iterations N" line converts the persistent PCG kernel's DRAM bytes to bytes per iteration)"""
 import collections
 import csv
@@ -14,6 +15,7 @@ import sys
 
 tag, scene, launches, rep = sys.argv[1:5]
 pcg_iters = None
+evalflops = sys.argv[6] if len(sys.argv) > 6 else None
 if len(sys.argv) > 5:
     m = re.search(r"pcg iterations (\d+)", open(sys.argv[5]).read())
     pcg_iters = int(m.group(1)) if m else None
@@ -104,6 +106,26 @@ if pp and pcg_iters:
     d[scene]["pcg_iterations"] = pcg_iters
     d[scene]["pcg_dram_bytes_per_iteration"] = 1e6 * (pp[0]["dram__bytes_read.sum"] +
                                                        pp[0]["dram__bytes_write.sum"]) / pcg_iters
+if evalflops and os.path.exists(evalflops):
+    t2 = open(evalflops).read()
+    rr = list(csv.reader(io.StringIO(t2[t2.find('"ID"'):])))
+    h2 = rr[0]
+    k2, m2, v2 = h2.index("Kernel Name"), h2.index("Metric Name"), h2.index("Metric Value")
+    cnt = collections.Counter()
+    for r in rr[1:]:
+        if len(r) > v2:
+            cnt[r[m2]] += float(r[v2].replace(",", ""))
+    dfma = cnt["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"]
+    dadd = cnt["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"]
+    dmul = cnt["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"]
+    d[scene]["eval_flops_per_step"] = 2 * dfma + dadd + dmul
+    d[scene]["eval_fp64_inst"] = {"dfma": dfma, "dadd": dadd, "dmul": dmul}
+    with open(os.path.join(out, f"{tag}_eval_flops_{scene}.md"), "w") as f:
+        f.write(f"# {tag}: FP64 work of the local evaluation, scene {scene} (one Newton step, every k_eval* launch)\n\n"
+                f"`ncu --metrics smsp__sass_thread_inst_executed_op_{{dfma,dadd,dmul}}_pred_on.sum -k regex:k_eval "
+                f"python tools/one_step.py {scene} 1`\n\n"
+                f"| DFMA | DADD | DMUL | FLOPs (2 DFMA + DADD + DMUL) |\n|---:|---:|---:|---:|\n"
+                f"| {dfma:.4g} | {dadd:.4g} | {dmul:.4g} | {2 * dfma + dadd + dmul:.4g} |\n")
 json.dump(d, open(js, "w"), indent=1)
 print("\n".join(lines[:16]))
 print("\n".join(tl))
