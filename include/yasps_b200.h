@@ -99,8 +99,12 @@ int ys_add_point_union(ys_context* ctx, int32_t n_children, const int32_t* domai
 /* Pair primitive with an arity-2 connectivity into a union (sim.cpp:445-447).
  * dynamic=1 marks a dynamic primitive (PrimitiveType(..., is_dynamic)). */
 int ys_add_pair_set(ys_context* ctx, int32_t union_id, int32_t dynamic, int32_t* pairset_id);
+/* A stencil primitive of arity 2, 3 or 4 into a union (a pair set is arity 2):
+ * the point-edge (3) and point-triangle / edge-edge (4) barriers below.  Not in
+ * the reference (its contact is point-point only, proj/README.md:110-111). */
+int ys_add_stencil_set(ys_context* ctx, int32_t union_id, int32_t arity, int32_t dynamic, int32_t* set_id);
 /* PrimitiveType::resize_dynamic (scene.cpp:171-199): replaces the pair table
- * (2*n union-global indices) and bumps the dynamic epoch. Static pair sets
+ * (arity*n union-global indices; 2*n for pair sets) and bumps the dynamic epoch. Static pair sets
  * may only be set before ys_finalize. */
 int ys_set_pairs(ys_context* ctx, int32_t pairset, int64_t n, const int64_t* pairs);
 int ys_pair_count(ys_context* ctx, int32_t pairset, int64_t* n);
@@ -127,6 +131,19 @@ int ys_add_stable_neo_hookean(ys_context* ctx, int32_t pos_target, int64_t n_tet
  * d squared distance, over a pair set. */
 int ys_add_point_point_barrier(ys_context* ctx, int32_t pairset, double dhat, double kappa,
                                double weight, int32_t mode, int32_t* energy_id);
+/* Point-triangle (stencil p, t0, t1, t2), edge-edge (a0, a1, b0, b1) and
+ * point-edge (p, e0, e1) barriers — NOT IN THE REFERENCE: weight kappa
+ * (d - dhat)^2 log(d / dhat)^2 (the point-point barrier of energies.cpp:30-47)
+ * on the squared distance d between the primitives, with IPC's distance types
+ * (point-plane / line-line / point-line / point-point by the closest-point
+ * region), FullProject.  Stencil sets of arity 4 / 4 / 3 over unions of free
+ * and fixed points. */
+int ys_add_point_triangle_barrier(ys_context* ctx, int32_t set, double dhat, double kappa, double weight,
+                                  int32_t* energy_id);
+int ys_add_edge_edge_barrier(ys_context* ctx, int32_t set, double dhat, double kappa, double weight,
+                             int32_t* energy_id);
+int ys_add_point_edge_barrier(ys_context* ctx, int32_t set, double dhat, double kappa, double weight,
+                              int32_t* energy_id);
 /* add_repulsive_energy (energies.cpp:20-28): weight / ||p0 - p1||. */
 int ys_add_repulsive(ys_context* ctx, int32_t pairset, double weight, int32_t mode,
                      int32_t* energy_id);

@@ -46,7 +46,7 @@
 #define MAXW 24
 #define MAXK 4
 
-enum { K_SNH = 0, K_BENDING, K_INERTIA, K_ORTHO, K_PP, K_REPULSIVE };
+enum { K_SNH = 0, K_BENDING, K_INERTIA, K_ORTHO, K_PP, K_REPULSIVE, K_PT, K_EE, K_PE };
 
 typedef struct {
   int64_t n;
@@ -71,6 +71,7 @@ typedef struct {
 
 typedef struct {
   int uni, dynamic;
+  int arity; /* points per instance: 2 pairs, 3 point-edge, 4 point-triangle / edge-edge */
   int64_t n;
   int64_t* pairs;
 } PairSet;
@@ -430,12 +431,12 @@ static void energy_slots(yo_context* c, const Energy* e, int64_t i, Slot* s) {
     case K_INERTIA:
       point_slots(c, &c->d[e->domain], i, 0, s);
       break;
-    default: {
+    default: { /* JoinRep(stencil2v, UnionSel): pairs (arity 2) and contact stencils */
       const PairSet* p = &c->ps[e->pairset];
       const Union* u = &c->u[p->uni];
-      for (int l = 0; l < 2; ++l) {
+      for (int l = 0; l < p->arity; ++l) {
         int64_t local;
-        const int br = union_decode(c, u, p->pairs[2 * i + l], &local);
+        const int br = union_decode(c, u, p->pairs[p->arity * i + l], &local);
         point_slots(c, &c->d[u->child[br]], local, l * u->width, s + l * u->kappa_u);
       }
     }
@@ -734,6 +735,165 @@ static void snh_psi(const Energy* e, int64_t t, Jet F[9], Jet* psi) {
 }
 
 /* Local energy / gradient / Hessian in the uncompressed width; vars = JN. */
+/* ------------------------------------------------------------------------
+ * Point-triangle / edge-edge / point-edge barriers — NOT IN THE REFERENCE
+ * (its contact is point-point only, proj/README.md:110-111), so this is the
+ * specification the B200 kernels are checked against (with finite
+ * differences and PSD checks): the point-point barrier of energies.cpp:30-47
+ * on the squared distance d between the stencil's primitives, IPC's distance
+ * types chosen on the current positions (Ericson, Real-Time Collision
+ * Detection 5.1.5 / 5.1.9), FullProject.
+ * ------------------------------------------------------------------------ */
+enum { CT_PP = 0, CT_PE = 1, CT_PT = 2, CT_EE = 3 };
+typedef struct {
+  int type, a, b, c, e;
+} ContactSel;
+
+static double c_dot(const double* x, const double* y) { return x[0] * y[0] + x[1] * y[1] + x[2] * y[2]; }
+static void c_sub(const double* x, const double* y, double* o) {
+  o[0] = x[0] - y[0];
+  o[1] = x[1] - y[1];
+  o[2] = x[2] - y[2];
+}
+static ContactSel csel(int t, int a, int b, int c, int e) {
+  ContactSel r = {t, a, b, c, e};
+  return r;
+}
+
+static ContactSel classify_pt(double x[4][3]) {
+  double ab[3], ac[3], ap[3], bp[3], cp[3];
+  c_sub(x[2], x[1], ab);
+  c_sub(x[3], x[1], ac);
+  c_sub(x[0], x[1], ap);
+  const double d1 = c_dot(ab, ap), d2 = c_dot(ac, ap);
+  if (d1 <= 0.0 && d2 <= 0.0) return csel(CT_PP, 0, 1, 0, 0);
+  c_sub(x[0], x[2], bp);
+  const double d3 = c_dot(ab, bp), d4 = c_dot(ac, bp);
+  if (d3 >= 0.0 && d4 <= d3) return csel(CT_PP, 0, 2, 0, 0);
+  const double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) return csel(CT_PE, 0, 1, 2, 0);
+  c_sub(x[0], x[3], cp);
+  const double d5 = c_dot(ab, cp), d6 = c_dot(ac, cp);
+  if (d6 >= 0.0 && d5 <= d6) return csel(CT_PP, 0, 3, 0, 0);
+  const double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) return csel(CT_PE, 0, 1, 3, 0);
+  const double va = d3 * d6 - d5 * d4;
+  if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) return csel(CT_PE, 0, 2, 3, 0);
+  return csel(CT_PT, 0, 1, 2, 3);
+}
+
+static ContactSel classify_pe(double x[4][3]) {
+  double ed[3], ap[3];
+  c_sub(x[2], x[1], ed);
+  c_sub(x[0], x[1], ap);
+  const double t = c_dot(ap, ed), ee = c_dot(ed, ed);
+  if (t <= 0.0) return csel(CT_PP, 0, 1, 0, 0);
+  if (t >= ee) return csel(CT_PP, 0, 2, 0, 0);
+  return csel(CT_PE, 0, 1, 2, 0);
+}
+
+static ContactSel classify_ee(double x[4][3]) {
+  double d1[3], d2[3], r[3];
+  c_sub(x[1], x[0], d1);
+  c_sub(x[3], x[2], d2);
+  c_sub(x[0], x[2], r);
+  const double a = c_dot(d1, d1), e = c_dot(d2, d2), f = c_dot(d2, r);
+  const double cc = c_dot(d1, r), b = c_dot(d1, d2);
+  const double denom = a * e - b * b;
+  double s;
+  int s_clamped;
+  if (denom > 1e-20 * (a * e)) {
+    s = (b * f - cc * e) / denom;
+    s_clamped = s <= 0.0 || s >= 1.0;
+    s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+  } else {
+    s = 0.0;
+    s_clamped = 1;
+  }
+  const double tn = b * s + f;
+  if (tn <= 0.0) {
+    const double sn = -cc;
+    s_clamped = sn <= 0.0 || sn >= a;
+    s = sn <= 0.0 ? 0.0 : (sn >= a ? 1.0 : sn / a);
+    if (s_clamped) return csel(CT_PP, s == 0.0 ? 0 : 1, 2, 0, 0);
+    return csel(CT_PE, 2, 0, 1, 0);
+  }
+  if (tn >= e) {
+    const double sn = b - cc;
+    s_clamped = sn <= 0.0 || sn >= a;
+    s = sn <= 0.0 ? 0.0 : (sn >= a ? 1.0 : sn / a);
+    if (s_clamped) return csel(CT_PP, s == 0.0 ? 0 : 1, 3, 0, 0);
+    return csel(CT_PE, 3, 0, 1, 0);
+  }
+  if (s_clamped) return csel(CT_PE, s == 0.0 ? 0 : 1, 2, 3, 0);
+  return csel(CT_EE, 0, 1, 2, 3);
+}
+
+static void j_dot3(Jet* o, const Jet* a, const Jet* b) {
+  Jet q;
+  j_mul(o, &a[0], &b[0]);
+  j_mul(&q, &a[1], &b[1]);
+  j_add(o, o, &q);
+  j_mul(&q, &a[2], &b[2]);
+  j_add(o, o, &q);
+}
+
+/* squared distance of the selected type over the stencil's point jets P */
+static void contact_dist2(ContactSel s, Jet (*P)[3], Jet* d) {
+  Jet u[3], v[3], w[3], n[3], sp, num, den;
+  int k;
+  if (s.type == CT_PP) {
+    for (k = 0; k < 3; ++k) j_sub(&u[k], &P[s.b][k], &P[s.a][k]);
+    j_dot3(d, u, u);
+  } else if (s.type == CT_PE) {
+    for (k = 0; k < 3; ++k) {
+      j_sub(&u[k], &P[s.b][k], &P[s.a][k]);
+      j_sub(&v[k], &P[s.c][k], &P[s.a][k]);
+      j_sub(&w[k], &P[s.c][k], &P[s.b][k]);
+    }
+    j_cross(n, u, v);
+    j_dot3(&num, n, n);
+    j_dot3(&den, w, w);
+    j_div(d, &num, &den);
+  } else if (s.type == CT_PT) {
+    for (k = 0; k < 3; ++k) {
+      j_sub(&u[k], &P[s.a][k], &P[s.b][k]);
+      j_sub(&v[k], &P[s.c][k], &P[s.b][k]);
+      j_sub(&w[k], &P[s.e][k], &P[s.b][k]);
+    }
+    j_cross(n, v, w);
+    j_dot3(&sp, u, n);
+    j_mul(&num, &sp, &sp);
+    j_dot3(&den, n, n);
+    j_div(d, &num, &den);
+  } else {
+    for (k = 0; k < 3; ++k) {
+      j_sub(&u[k], &P[s.b][k], &P[s.a][k]);
+      j_sub(&v[k], &P[s.e][k], &P[s.c][k]);
+      j_sub(&w[k], &P[s.c][k], &P[s.a][k]);
+    }
+    j_cross(n, u, v);
+    j_dot3(&sp, w, n);
+    j_mul(&num, &sp, &sp);
+    j_dot3(&den, n, n);
+    j_div(d, &num, &den);
+  }
+}
+
+/* w kappa (d - dhat)^2 log(d / dhat)^2 on a jet d (energies.cpp:30-39) */
+static void pp_barrier(const Energy* e, const Jet* d, Jet* E) {
+  Jet i5, len, lg, acc;
+  j_scale(&i5, d, 1.0 / e->prm[0]);
+  i5.v = d->v / e->prm[0];
+  j_addc(&len, d, -e->prm[0]);
+  j_log(&lg, &i5);
+  j_mul(&acc, &len, &len);
+  j_scale(&acc, &acc, e->prm[1]);
+  j_mul(&acc, &acc, &lg);
+  j_mul(&acc, &acc, &lg);
+  j_scale(E, &acc, e->prm[2]);
+}
+
 static void local_eval(yo_context* c, const Energy* e, int64_t i, const double* X, Jet* E) {
   switch (e->kind) {
     case K_SNH: {
@@ -804,6 +964,24 @@ static void local_eval(yo_context* c, const Energy* e, int64_t i, const double* 
         j_add(&acc, &acc, &q);
       }
       j_scale(E, &acc, 0.5 * e->cdata[i]);
+      break;
+    }
+    case K_PT:
+    case K_EE:
+    case K_PE: {
+      const PairSet* ps = &c->ps[e->pairset];
+      const Union* u = &c->u[ps->uni];
+      Jet P[4][3], d;
+      double xv[4][3];
+      for (int l = 0; l < ps->arity; ++l) {
+        int64_t loc;
+        const int br = union_decode(c, u, ps->pairs[ps->arity * i + l], &loc);
+        point_jets(c, &c->d[u->child[br]], loc, l * u->width, X, P[l]);
+        point_value(c, &c->d[u->child[br]], loc, X, xv[l]);
+      }
+      const ContactSel sel = e->kind == K_PT ? classify_pt(xv) : e->kind == K_EE ? classify_ee(xv) : classify_pe(xv);
+      contact_dist2(sel, P, &d);
+      pp_barrier(e, &d, E);
       break;
     }
     default: {
@@ -1741,16 +1919,22 @@ int yo_add_point_union(yo_context* c, int32_t n, const int32_t* doms, int32_t* i
   API_END;
 }
 
-int yo_add_pair_set(yo_context* c, int32_t uni, int32_t dynamic, int32_t* id) {
+int yo_add_stencil_set(yo_context* c, int32_t uni, int32_t arity, int32_t dynamic, int32_t* id) {
   API_BEGIN(c);
-  require_not_fin(c, "ys_add_pair_set");
+  require_not_fin(c, "ys_add_stencil_set");
   if (uni < 0 || uni >= c->nu) fail(c, YS_ERR_DECL, "unknown primitive union");
+  if (arity < 2 || arity > 4) fail(c, YS_ERR_DECL, "stencil arity must be 2, 3 or 4");
   GROW(c->ps, c->nps);
   memset(&c->ps[c->nps], 0, sizeof(PairSet));
   c->ps[c->nps].uni = uni;
+  c->ps[c->nps].arity = arity;
   c->ps[c->nps].dynamic = dynamic != 0;
   *id = c->nps++;
   API_END;
+}
+
+int yo_add_pair_set(yo_context* c, int32_t uni, int32_t dynamic, int32_t* id) {
+  return yo_add_stencil_set(c, uni, 2, dynamic, id);
 }
 
 int yo_set_pairs(yo_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
@@ -1761,13 +1945,13 @@ int yo_set_pairs(yo_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
   if (n < 0) fail(c, YS_ERR_VALIDATION, "negative instance count");
   int64_t total = 0;
   for (int k = 0; k < c->u[p->uni].nchild; ++k) total += c->d[c->u[p->uni].child[k]].n;
-  for (int64_t k = 0; k < 2 * n; ++k)
+  for (int64_t k = 0; k < p->arity * n; ++k)
     if (pairs[k] < 0 || pairs[k] >= total)
       fail(c, YS_ERR_VALIDATION, "connectivity 'pp2v': index %lld at position %lld out of range [0, %lld)",
            (long long)pairs[k], (long long)k, (long long)total);
   free(p->pairs);
-  p->pairs = xcalloc((size_t)(2 * n), sizeof(int64_t));
-  memcpy(p->pairs, pairs, sizeof(int64_t) * (size_t)(2 * n));
+  p->pairs = xcalloc((size_t)(p->arity * n), sizeof(int64_t));
+  memcpy(p->pairs, pairs, sizeof(int64_t) * (size_t)(p->arity * n));
   p->n = n;
   c->epoch++;
   API_END;
@@ -1783,7 +1967,7 @@ int yo_pair_count(yo_context* c, int32_t ps, int64_t* n) {
 int yo_get_pairs(yo_context* c, int32_t ps, int64_t* out) {
   API_BEGIN(c);
   if (ps < 0 || ps >= c->nps) fail(c, YS_ERR_DECL, "unknown pair set");
-  memcpy(out, c->ps[ps].pairs, sizeof(int64_t) * (size_t)(2 * c->ps[ps].n));
+  memcpy(out, c->ps[ps].pairs, sizeof(int64_t) * (size_t)(c->ps[ps].arity * c->ps[ps].n));
   API_END;
 }
 
@@ -1793,6 +1977,7 @@ int yo_refresh_pairs(yo_context* c, int32_t ps, double dhat, const int32_t* chil
   require_fin(c);
   if (ps < 0 || ps >= c->nps) fail(c, YS_ERR_DECL, "unknown pair set");
   PairSet* p = &c->ps[ps];
+  if (p->arity != 2) fail(c, YS_ERR_DECL, "ys_refresh_pairs: point-point pair sets only");
   const Union* u = &c->u[p->uni];
   int64_t total = 0;
   for (int k = 0; k < u->nchild; ++k) total += c->d[u->child[k]].n;
@@ -1988,6 +2173,43 @@ static int add_pair(yo_context* c, int kind, int32_t ps, double dhat, double kap
   e.prm[2] = weight;
   *id = add_energy(c, &e);
   API_END;
+}
+
+static int add_contact(yo_context* c, int kind, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  API_BEGIN(c);
+  require_not_fin(c, kind == K_PT ? "point_triangle" : kind == K_EE ? "edge_edge" : "point_edge");
+  if (ps < 0 || ps >= c->nps) fail(c, YS_ERR_DECL, "unknown stencil set");
+  const int want = kind == K_PE ? 3 : 4;
+  const char* nm = kind == K_PT ? "point_triangle" : kind == K_EE ? "edge_edge" : "point_edge";
+  if (c->ps[ps].arity != want) fail(c, YS_ERR_DECL, "%s needs a stencil set of arity %d", nm, want);
+  const Union* u = &c->u[c->ps[ps].uni];
+  if (u->kappa_u != 1) fail(c, YS_ERR_DECL, "%s: unions of free and fixed points only", nm);
+  if (!(dhat > 0.0)) fail(c, YS_ERR_VALIDATION, "dhat must be positive");
+  Energy e;
+  memset(&e, 0, sizeof(e));
+  e.kind = kind;
+  e.dynamic = c->ps[ps].dynamic;
+  e.mode = YS_PROJECT_FULL;
+  e.pairset = ps;
+  e.target = e.domain = -1;
+  e.n = c->ps[ps].n;
+  e.kappa = want;
+  e.width = 3 * want;
+  e.prm[0] = dhat;
+  e.prm[1] = kappa;
+  e.prm[2] = weight;
+  *id = add_energy(c, &e);
+  API_END;
+}
+
+int yo_add_point_triangle_barrier(yo_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact(c, K_PT, ps, dhat, kappa, weight, id);
+}
+int yo_add_edge_edge_barrier(yo_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact(c, K_EE, ps, dhat, kappa, weight, id);
+}
+int yo_add_point_edge_barrier(yo_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact(c, K_PE, ps, dhat, kappa, weight, id);
 }
 
 int yo_add_point_point_barrier(yo_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t mode,

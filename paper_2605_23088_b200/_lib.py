@@ -90,6 +90,7 @@ _SIGS = {
     "get_points": [_P, _I32, _PD],
     "add_point_union": [_P, _I32, _PI32, _PI32],
     "add_pair_set": [_P, _I32, _I32, _PI32],
+    "add_stencil_set": [_P, _I32, _I32, _I32, _PI32],
     "set_pairs": [_P, _I32, _I64, _PI64],
     "pair_count": [_P, _I32, _PI64],
     "get_pairs": [_P, _I32, _PI64],
@@ -97,6 +98,9 @@ _SIGS = {
     "add_stable_neo_hookean": [_P, _I32, _I64, _PI64, _PD, _D, _D, _D, _I32, _PI32],
     "add_point_point_barrier": [_P, _I32, _D, _D, _D, _I32, _PI32],
     "add_repulsive": [_P, _I32, _D, _I32, _PI32],
+    "add_point_triangle_barrier": [_P, _I32, _D, _D, _D, _PI32],
+    "add_edge_edge_barrier": [_P, _I32, _D, _D, _D, _PI32],
+    "add_point_edge_barrier": [_P, _I32, _D, _D, _D, _PI32],
     "add_inertia": [_P, _I32, _PD, _PD, _PI32],
     "set_inertia_anchor": [_P, _I32, _PD],
     "add_affine_orthogonality": [_P, _I32, _D, _D, _PI32],

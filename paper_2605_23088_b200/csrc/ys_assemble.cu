@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "ys_contact4.cuh"
 #include "ys_device.cuh"
 
 namespace ys {
@@ -65,6 +66,7 @@ EnergyDev energy_dev(Context& c, Energy& e) {
     E.uni.child = u.d_child.p;
     E.uni.offsets = u.d_offsets.p;
     E.pairs = ps.pairs.p;
+    E.arity = ps.arity;
   }
   for (int k = 0; k < 6; ++k) E.prm[k] = e.prm[k];
   E.slots = e.slots.p;
@@ -367,6 +369,98 @@ __global__ void k_eval_point(EnergyDev E, const double* __restrict__ X, int proj
   point_instance(E, i, X, project, want_h, hc, gc, err);
 }
 
+// Point-triangle / edge-edge / point-edge barriers over a union of free and
+// fixed points (ys_contact4.cuh): distance type on the current positions, the
+// type's squared distance as a jet over the 3 A stencil coordinates, the
+// point-point barrier's b(d) composed on it, then exactly the reference's
+// assemble_local FullProject route (assembly.cpp:284-321): raw-slot gradient,
+// local_compress, symmetrise, psd_project of the m x m block.
+__device__ __forceinline__ void stencil_points(const EnergyDev& E, int64_t i, const double* __restrict__ X,
+                                               double (*x)[3]) {
+  for (int l = 0; l < E.arity; ++l) {
+    int64_t loc;
+    const int br = union_decode(E.uni, E.pairs[int64_t(E.arity) * i + l], &loc);
+    point_position(E.uni.child[br], loc, X, x[l]);
+  }
+}
+
+template <int A>
+__global__ void __launch_bounds__(128) k_eval_contact(EnergyDev E, const double* __restrict__ X, int project,
+                                                      int want_h, double* __restrict__ hc, double* __restrict__ gc,
+                                                      int* err) {
+  constexpr int N = 3 * A;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= E.n) return;
+  double x[4][3];
+  stencil_points(E, i, X, x);
+  const ContactSel sel = classify_contact(E.kind, x);
+  Jet<N> d;
+  contact_dist2<N>(sel, x, d);
+  const PairParams PP{E.prm[0], E.prm[1], E.prm[2], 0};
+  double b, b1, b2;
+  const int st = pair_b(d.v, PP, &b, &b1, &b2);
+  if (st) atomicOr(err, st == 1 ? kErrLog : kErrDiv);
+  PSlot s[kMaxKappa];
+  energy_slots(E, i, s);
+  // raw-slot gradient: g = b'(d) grad d
+  double* go = gc + inst_goff(E, i);
+  int o = 0;
+  for (int l = 0; l < A; ++l) {
+    if (s[l].gstart < 0) continue;
+    for (int k = 0; k < 3; ++k) go[o + k] = b1 * d.g[3 * l + k];
+    o += 3;
+  }
+  if (!want_h) return;
+  UBlocks u;
+  make_ublocks(s, A, u);
+  int ub_of[4];
+  for (int l = 0; l < A; ++l) {
+    ub_of[l] = -1;
+    for (int q = 0; q < u.nu; ++q)
+      if (s[l].gstart >= 0 && u.gstart[q] == s[l].gstart) ub_of[l] = q;
+  }
+  const int m = 3 * u.nu;
+  double Hc[144];
+  for (int k = 0; k < m * m; ++k) Hc[k] = 0.0;
+  // local_compress of H = b'(d) hess d + b''(d) grad d grad d^T (symmetric)
+  for (int l = 0; l < A; ++l) {
+    if (ub_of[l] < 0) continue;
+    for (int lp = 0; lp < A; ++lp) {
+      if (ub_of[lp] < 0) continue;
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q) {
+          const int ir = 3 * l + r, iq = 3 * lp + q;
+          Hc[(3 * ub_of[l] + r) * m + 3 * ub_of[lp] + q] += b1 * d.h[jh<N>(ir, iq)] + b2 * d.g[ir] * d.g[iq];
+        }
+    }
+  }
+  if (project) psd_project_dense(Hc, m);
+  // ublock-pair blocks (a <= b), oriented so gstart(lo) <= gstart(hi)
+  double* h = hc + inst_hoff(E, i);
+  int64_t off = 0;
+  for (int a = 0; a < u.nu; ++a)
+    for (int bb = a; bb < u.nu; ++bb) {
+      const bool sw = u.gstart[a] > u.gstart[bb];
+      const int lo = sw ? bb : a, hi = sw ? a : bb;
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q) h[off + 3 * r + q] = Hc[(3 * lo + r) * m + 3 * hi + q];
+      off += 9;
+    }
+}
+
+__device__ __forceinline__ double contact_energy(const EnergyDev& E, int64_t i, const double* __restrict__ X,
+                                                 int* err) {
+  double x[4][3];
+  stencil_points(E, i, X, x);
+  const ContactSel sel = classify_contact(E.kind, x);
+  const double d = contact_dist2_value(sel, x);
+  const PairParams PP{E.prm[0], E.prm[1], E.prm[2], 0};
+  double b, b1, b2;
+  const int st = pair_b(d, PP, &b, &b1, &b2);
+  if (st) atomicOr(err, st == 1 ? kErrLog : kErrDiv);
+  return b;
+}
+
 // Many small energies of one kind (C3: 64 affine bodies, each with its own
 // orthogonality and inertia energy of one / 27 instances) in one launch:
 // thread t -> energy j (prefix[j] <= t < prefix[j + 1]), instance t - prefix[j].
@@ -434,6 +528,11 @@ __global__ void k_energy(EnergyDev E, const double* __restrict__ X, double* __re
       e = 0.5 * E.cdata[i] * d2;
       break;
     }
+    case K_PT:
+    case K_EE:
+    case K_PE:
+      e = contact_energy(E, i, X, err);
+      break;
     default: {
       double p0[3], p1[3];
       int64_t l0, l1;
@@ -870,6 +969,15 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
           multi[e.dynamic ? 1 : 0][1].push_back(id);
           continue;
         }
+        break;
+      case K_PT:
+      case K_EE:
+        k_eval_contact<4><<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                              c.errflag.p);
+        break;
+      case K_PE:
+        k_eval_contact<3><<<grid_for(e.n, 128), 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p,
+                                                              c.errflag.p);
         break;
       default:
         if (E.uni.kappa_u == 1)

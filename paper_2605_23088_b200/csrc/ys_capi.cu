@@ -39,6 +39,9 @@ const char* kind_name(int k) {
     case K_ORTHO: return "affine_orthogonality";
     case K_PP: return "point_point";
     case K_REPULSIVE: return "repulsive";
+    case K_PT: return "point_triangle";
+    case K_EE: return "edge_edge";
+    case K_PE: return "point_edge";
   }
   return "?";
 }
@@ -285,7 +288,7 @@ double elapsed(std::chrono::steady_clock::time_point t0) {
 void check_pairs_in_range(Context& c, PairSet& ps, int64_t n, const int64_t* pairs) {
   int64_t total = 0;
   for (int32_t d : c.unions[ps.uni].children) total += c.domains[d].n;
-  for (int64_t k = 0; k < 2 * n; ++k)
+  for (int64_t k = 0; k < int64_t(ps.arity) * n; ++k)
     if (pairs[k] < 0 || pairs[k] >= total)
       fail(YS_ERR_VALIDATION, "connectivity 'pp2v': index " + std::to_string(pairs[k]) + " at position " +
                                   std::to_string(k) + " out of range [0, " + std::to_string(total) + ")");
@@ -468,16 +471,22 @@ int ys_add_point_union(ys_context* c, int32_t n, const int32_t* doms, int32_t* i
   });
 }
 
-int ys_add_pair_set(ys_context* c, int32_t uni, int32_t dynamic, int32_t* id) {
+int ys_add_stencil_set(ys_context* c, int32_t uni, int32_t arity, int32_t dynamic, int32_t* id) {
   return guarded(c, [&] {
-    require_not_finalized(*c, "ys_add_pair_set");
+    require_not_finalized(*c, "ys_add_stencil_set");
     if (uni < 0 || uni >= int32_t(c->unions.size())) fail(YS_ERR_DECL, "unknown primitive union");
+    if (arity < 2 || arity > 4) fail(YS_ERR_DECL, "stencil arity must be 2, 3 or 4");
     PairSet p;
     p.uni = uni;
+    p.arity = arity;
     p.dynamic = dynamic != 0;
     c->pairsets.push_back(std::move(p));
     *id = int32_t(c->pairsets.size() - 1);
   });
+}
+
+int ys_add_pair_set(ys_context* c, int32_t uni, int32_t dynamic, int32_t* id) {
+  return ys_add_stencil_set(c, uni, 2, dynamic, id);
 }
 
 int ys_set_pairs(ys_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
@@ -491,12 +500,12 @@ int ys_set_pairs(ys_context* c, int32_t ps, int64_t n, const int64_t* pairs) {
     if (c->finalized) {
       // the device copy is authoritative; ys_get_pairs downloads it lazily.  The
       // pageable upload has staged q before returning, so no synchronisation.
-      std::vector<int32_t> q(pairs, pairs + 2 * n);
+      std::vector<int32_t> q(pairs, pairs + int64_t(p.arity) * n);
       p.pairs.upload(q, c->stream);
       p.h_pairs.clear();
       p.host_stale = n > 0;
     } else {
-      p.h_pairs.assign(pairs, pairs + 2 * n);
+      p.h_pairs.assign(pairs, pairs + int64_t(p.arity) * n);
       p.host_stale = false;
     }
     ++c->epoch;  // Scene::bump_dynamic_epoch (scene.cpp:198)
@@ -516,7 +525,7 @@ int ys_get_pairs(ys_context* c, int32_t ps, int64_t* out) {
     PairSet& p = c->pairsets[ps];
     if (p.host_stale) {
       std::vector<int32_t> h = p.pairs.to_host(c->stream);
-      p.h_pairs.assign(h.begin(), h.begin() + 2 * p.n);
+      p.h_pairs.assign(h.begin(), h.begin() + int64_t(p.arity) * p.n);
       p.host_stale = false;
     }
     std::copy(p.h_pairs.begin(), p.h_pairs.end(), out);
@@ -528,6 +537,7 @@ int ys_refresh_pairs(ys_context* c, int32_t ps, double dhat, const int32_t* chil
     require_finalized(*c);
     if (ps < 0 || ps >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown pair set");
     if (!c->pairsets[ps].dynamic) fail(YS_ERR_VALIDATION, "resize_dynamic on static primitive contact.pp");
+    if (c->pairsets[ps].arity != 2) fail(YS_ERR_DECL, "ys_refresh_pairs: point-point pair sets only");
     ctx_refresh_pairs(*c, ps, dhat, child_is_fixed, n);
   });
 }
@@ -700,6 +710,47 @@ static int add_pair_energy(ys_context* c, int kind, int32_t ps, double dhat, dou
     e.prm[2] = weight;
     *id = add_energy(*c, std::move(e));
   });
+}
+
+// Point-triangle / edge-edge / point-edge barriers (ys_contact4.cuh; not in
+// the reference): a stencil set of arity 4 / 4 / 3 over a union of free and
+// fixed points, the point-point barrier's b(d) on the squared distance,
+// FullProject.
+static int add_contact_energy(ys_context* c, int kind, int32_t ps, double dhat, double kappa, double weight,
+                              int32_t* id) {
+  return guarded(c, [&] {
+    require_not_finalized(*c, kind_name(kind));
+    if (ps < 0 || ps >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown stencil set");
+    const PairSet& p = c->pairsets[ps];
+    const int want = kind == K_PE ? 3 : 4;
+    if (p.arity != want)
+      fail(YS_ERR_DECL, std::string(kind_name(kind)) + " needs a stencil set of arity " + std::to_string(want));
+    const Union& u = c->unions[p.uni];
+    if (u.kappa_u != 1) fail(YS_ERR_DECL, std::string(kind_name(kind)) + ": unions of free and fixed points only");
+    if (!(dhat > 0.0)) fail(YS_ERR_VALIDATION, "dhat must be positive");
+    Energy e;
+    e.kind = kind;
+    e.dynamic = p.dynamic;
+    e.mode = YS_PROJECT_FULL;
+    e.pairset = ps;
+    e.n = p.n;
+    e.kappa = p.arity;
+    e.width = 3 * p.arity;
+    e.prm[0] = dhat;
+    e.prm[1] = kappa;
+    e.prm[2] = weight;
+    *id = add_energy(*c, std::move(e));
+  });
+}
+
+int ys_add_point_triangle_barrier(ys_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact_energy(c, K_PT, ps, dhat, kappa, weight, id);
+}
+int ys_add_edge_edge_barrier(ys_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact_energy(c, K_EE, ps, dhat, kappa, weight, id);
+}
+int ys_add_point_edge_barrier(ys_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t* id) {
+  return add_contact_energy(c, K_PE, ps, dhat, kappa, weight, id);
 }
 
 int ys_add_point_point_barrier(ys_context* c, int32_t ps, double dhat, double kappa, double weight, int32_t mode,

@@ -22,7 +22,10 @@ enum Kind : int32_t {
   K_INERTIA = 2,   // add_inertia (energies.cpp:168-174)
   K_ORTHO = 3,     // add_affine_orthogonality (energies.cpp:120-127)
   K_PP = 4,        // add_point_point_barrier (energies.cpp:30-47)
-  K_REPULSIVE = 5  // add_repulsive_energy (energies.cpp:20-28)
+  K_REPULSIVE = 5, // add_repulsive_energy (energies.cpp:20-28)
+  K_PT = 6,        // point-triangle barrier (not in the reference; ys_contact4.cuh)
+  K_EE = 7,        // edge-edge barrier (not in the reference)
+  K_PE = 8         // point-edge barrier (not in the reference)
 };
 
 const char* kind_name(int k);
@@ -56,6 +59,7 @@ struct Union {
 
 struct PairSet {
   int32_t uni = -1;
+  int32_t arity = 2;  // points per instance: 2 (pairs), 3 (point-edge), 4 (point-triangle, edge-edge)
   bool dynamic = false;
   int64_t n = 0;
   std::vector<int64_t> h_pairs;

@@ -22,7 +22,7 @@ struct EnergyDev {
   const double* cdata;   // SNH: Binv+vol (10/inst); bending: c=k*w*l0 (1/inst); inertia: mass
   const double* anchor;  // inertia x_tilde
   int32_t startP;        // SNH/bending position target start; ortho amat target start
-  int32_t pad;
+  int32_t arity;         // stencil energies over a union: points per instance
   DomainDev dom;         // inertia domain
   UnionDev uni;          // pair energies
   const int32_t* pairs;  // pair energies: 2n union-global ids
@@ -119,6 +119,16 @@ __device__ __forceinline__ void energy_slots(const EnergyDev& E, int64_t i, PSlo
     case K_INERTIA:
       point_slots(E.dom, i, 0, 1.0, s);
       break;
+    case K_PT:
+    case K_EE:
+    case K_PE: {  // stencil energies over a union of free / fixed points (kappa_u = 1)
+      for (int l = 0; l < E.arity && l < kMaxKappa; ++l) {
+        int64_t local;
+        const int br = union_decode(E.uni, E.pairs[int64_t(E.arity) * i + l], &local);
+        point_slots(E.uni.child[br], local, 3 * l, 1.0, s + l);
+      }
+      break;
+    }
     default: {  // pair energies: JoinRep(pp2v, UnionSel)
       const int ku = E.uni.kappa_u;
 #pragma unroll

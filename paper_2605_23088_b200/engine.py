@@ -156,6 +156,7 @@ class Engine:
         self.ctx = h
         self.targets: list[tuple[int, int]] = []
         self.energy_names: list[str] = []
+        self._arity: dict[int, int] = {}
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -218,11 +219,20 @@ class Engine:
     def add_pair_set(self, union_id: int, dynamic: bool = True) -> int:
         pid = C.c_int32()
         self._c(self.f["add_pair_set"](self.ctx, union_id, 1 if dynamic else 0, C.byref(pid)))
+        self._arity[pid.value] = 2
+        return pid.value
+
+    def add_stencil_set(self, union_id: int, arity: int, dynamic: bool = True) -> int:
+        """A stencil primitive of arity 2-4 into a union (contact stencils of the
+        point-edge / point-triangle / edge-edge barriers; not in the reference)."""
+        pid = C.c_int32()
+        self._c(self.f["add_stencil_set"](self.ctx, union_id, int(arity), 1 if dynamic else 0, C.byref(pid)))
+        self._arity[pid.value] = int(arity)
         return pid.value
 
     def set_pairs(self, pairset: int, pairs):
         p = _i64(pairs)
-        self._c(self.f["set_pairs"](self.ctx, pairset, len(p) // 2, _ip64(p)))
+        self._c(self.f["set_pairs"](self.ctx, pairset, len(p) // self._arity.get(pairset, 2), _ip64(p)))
 
     def pair_count(self, pairset: int) -> int:
         n = C.c_int64()
@@ -231,10 +241,11 @@ class Engine:
 
     def get_pairs(self, pairset: int) -> np.ndarray:
         n = self.pair_count(pairset)
-        out = np.zeros(2 * n, dtype=np.int64)
+        a = self._arity.get(pairset, 2)
+        out = np.zeros(a * n, dtype=np.int64)
         if n:
             self._c(self.f["get_pairs"](self.ctx, pairset, _ip64(out)))
-        return out.reshape(n, 2)
+        return out.reshape(n, a)
 
     def refresh_pairs(self, pairset: int, dhat: float, child_is_fixed=None) -> int:
         n = C.c_int64()
@@ -259,6 +270,23 @@ class Engine:
                                                  float(youngs), float(poisson), float(weight),
                                                  1 if via_deformation_gradient else 0, C.byref(e)))
         return self._eid("stable_neo_hookean", e)
+
+    def _contact(self, fn: str, name: str, stencils: int, dhat: float, kappa: float, weight: float) -> int:
+        e = C.c_int32()
+        self._c(self.f[fn](self.ctx, stencils, float(dhat), float(kappa), float(weight), C.byref(e)))
+        return self._eid(name, e)
+
+    def add_point_triangle_barrier(self, stencils: int, dhat: float, kappa: float, weight: float = 1.0) -> int:
+        """Point-triangle barrier over an arity-4 stencil set (p, t0, t1, t2); not in the reference."""
+        return self._contact("add_point_triangle_barrier", "point_triangle", stencils, dhat, kappa, weight)
+
+    def add_edge_edge_barrier(self, stencils: int, dhat: float, kappa: float, weight: float = 1.0) -> int:
+        """Edge-edge barrier over an arity-4 stencil set (a0, a1, b0, b1); not in the reference."""
+        return self._contact("add_edge_edge_barrier", "edge_edge", stencils, dhat, kappa, weight)
+
+    def add_point_edge_barrier(self, stencils: int, dhat: float, kappa: float, weight: float = 1.0) -> int:
+        """Point-edge barrier over an arity-3 stencil set (p, e0, e1); not in the reference."""
+        return self._contact("add_point_edge_barrier", "point_edge", stencils, dhat, kappa, weight)
 
     def add_point_point_barrier(self, pairset: int, dhat: float, kappa: float, weight: float = 1.0,
                                 mode: int = YS_PROJECT_FULL) -> int:
