@@ -103,6 +103,16 @@ int ys_add_pair_set(ys_context* ctx, int32_t union_id, int32_t dynamic, int32_t*
  * the point-edge (3) and point-triangle / edge-edge (4) barriers below.  Not in
  * the reference (its contact is point-point only, proj/README.md:110-111). */
 int ys_add_stencil_set(ys_context* ctx, int32_t union_id, int32_t arity, int32_t dynamic, int32_t* set_id);
+/* Candidate primitives of a contact stencil set (not in the reference):
+ * kind 1 PT (prims_a: n_a points, prims_b: n_b triangles of 3 points),
+ * kind 2 EE (prims_a: n_a edges of 2 points; self-contact, prims_b ignored),
+ * kind 3 PE (prims_a: n_a points, prims_b: n_b edges); union indices. */
+int ys_set_stencil_primitives(ys_context* ctx, int32_t set, int32_t kind, int64_t n_a, const int64_t* prims_a,
+                              int64_t n_b, const int64_t* prims_b);
+/* The contact candidates on the device: every (a, b) (EE: b > a) sharing no
+ * point, not all points fixed, with the squared distance of its IPC distance
+ * type strictly below dhat, in (a, b) order; then resize_dynamic. */
+int ys_refresh_stencils(ys_context* ctx, int32_t set, double dhat, int64_t* n_stencils);
 /* PrimitiveType::resize_dynamic (scene.cpp:171-199): replaces the pair table
  * (arity*n union-global indices; 2*n for pair sets) and bumps the dynamic epoch. Static pair sets
  * may only be set before ys_finalize. */

@@ -74,6 +74,10 @@ typedef struct {
   int arity; /* points per instance: 2 pairs, 3 point-edge, 4 point-triangle / edge-edge */
   int64_t n;
   int64_t* pairs;
+  /* contact candidates (yo_set_stencil_primitives): kind 1 PT, 2 EE (self), 3 PE */
+  int pkind, aa, ab;
+  int64_t na, nb;
+  int64_t *pa, *pb;
 } PairSet;
 
 typedef struct {
@@ -827,6 +831,42 @@ static ContactSel classify_ee(double x[4][3]) {
   }
   if (s_clamped) return csel(CT_PE, s == 0.0 ? 0 : 1, 2, 3, 0);
   return csel(CT_EE, 0, 1, 2, 3);
+}
+
+/* value-only squared distance of the selected type: the same operations in
+ * the same order as the B200 candidate test (ys_contact4.cuh contact_dist2_value) */
+static void c_cross(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+static double contact_dist2_value(ContactSel s, double x[4][3]) {
+  double u[3], v[3], w[3], n[3];
+  if (s.type == CT_PP) {
+    c_sub(x[s.b], x[s.a], u);
+    return c_dot(u, u);
+  }
+  if (s.type == CT_PE) {
+    c_sub(x[s.b], x[s.a], u);
+    c_sub(x[s.c], x[s.a], v);
+    c_sub(x[s.c], x[s.b], w);
+    c_cross(u, v, n);
+    return c_dot(n, n) / c_dot(w, w);
+  }
+  if (s.type == CT_PT) {
+    c_sub(x[s.a], x[s.b], u);
+    c_sub(x[s.c], x[s.b], v);
+    c_sub(x[s.e], x[s.b], w);
+    c_cross(v, w, n);
+    const double sp = c_dot(u, n);
+    return (sp * sp) / c_dot(n, n);
+  }
+  c_sub(x[s.b], x[s.a], u);
+  c_sub(x[s.e], x[s.c], v);
+  c_sub(x[s.c], x[s.a], w);
+  c_cross(u, v, n);
+  const double sp = c_dot(w, n);
+  return (sp * sp) / c_dot(n, n);
 }
 
 static void j_dot3(Jet* o, const Jet* a, const Jet* b) {
@@ -1930,6 +1970,94 @@ int yo_add_stencil_set(yo_context* c, int32_t uni, int32_t arity, int32_t dynami
   c->ps[c->nps].arity = arity;
   c->ps[c->nps].dynamic = dynamic != 0;
   *id = c->nps++;
+  API_END;
+}
+
+/* Contact candidates of the PT / EE / PE barriers (not in the reference; its
+ * candidates are point-point only, sim.cpp:456-484): the all-pairs loop that
+ * specifies the B200 grid search (ys_stencil.cu).  Every (a, b) (EE: b > a)
+ * sharing no point, not all points fixed, with the squared distance of its
+ * distance type strictly below dhat, in (a, b) order. */
+int yo_set_stencil_primitives(yo_context* c, int32_t set, int32_t kind, int64_t n_a, const int64_t* prims_a,
+                              int64_t n_b, const int64_t* prims_b) {
+  API_BEGIN(c);
+  if (set < 0 || set >= c->nps) fail(c, YS_ERR_DECL, "unknown stencil set");
+  PairSet* p = &c->ps[set];
+  if (kind < 1 || kind > 3) fail(c, YS_ERR_VALIDATION, "stencil kind must be 1 (PT), 2 (EE) or 3 (PE)");
+  const int aa = kind == 2 ? 2 : 1, ab = kind == 1 ? 3 : 2;
+  if (aa + ab != p->arity) fail(c, YS_ERR_DECL, "stencil kind does not match the set's arity");
+  if (kind == 2) n_b = 0;
+  free(p->pa);
+  free(p->pb);
+  p->pa = xcalloc((size_t)(n_a * aa), sizeof(int64_t));
+  p->pb = xcalloc((size_t)(n_b * ab), sizeof(int64_t));
+  memcpy(p->pa, prims_a, sizeof(int64_t) * (size_t)(n_a * aa));
+  if (n_b) memcpy(p->pb, prims_b, sizeof(int64_t) * (size_t)(n_b * ab));
+  p->pkind = kind;
+  p->aa = aa;
+  p->ab = ab;
+  p->na = n_a;
+  p->nb = n_b;
+  API_END;
+}
+
+int yo_refresh_stencils(yo_context* c, int32_t set, double dhat, int64_t* out_n) {
+  API_BEGIN(c);
+  require_fin(c);
+  if (set < 0 || set >= c->nps) fail(c, YS_ERR_DECL, "unknown stencil set");
+  PairSet* p = &c->ps[set];
+  if (!p->pkind) fail(c, YS_ERR_VALIDATION, "stencil set has no primitives (ys_set_stencil_primitives)");
+  const Union* u = &c->u[p->uni];
+  int64_t total = 0;
+  for (int k = 0; k < u->nchild; ++k) total += c->d[u->child[k]].n;
+  double* pts = xcalloc((size_t)(3 * total), sizeof(double));
+  char* fixed = xcalloc((size_t)total, 1);
+  int64_t acc = 0;
+  for (int k = 0; k < u->nchild; ++k) {
+    const Domain* d = &c->d[u->child[k]];
+    for (int64_t i = 0; i < d->n; ++i) {
+      point_value(c, d, i, c->X, pts + 3 * (acc + i));
+      fixed[acc + i] = d->kind == YS_POINTS_FIXED;
+    }
+    acc += d->n;
+  }
+  const int self = p->pkind == 2, ar = p->aa + p->ab;
+  const int kind = p->pkind == 1 ? K_PT : p->pkind == 2 ? K_EE : K_PE;
+  const int64_t* B = self ? p->pa : p->pb;
+  const int64_t nb = self ? p->na : p->nb;
+  const int abb = self ? p->aa : p->ab;
+  int64_t cnt = 0, cap = 256;
+  int64_t* idx = xcalloc((size_t)(ar * cap), sizeof(int64_t));
+  for (int64_t a = 0; a < p->na; ++a)
+    for (int64_t b = self ? a + 1 : 0; b < nb; ++b) {
+      int64_t st[4];
+      int shared = 0, allfixed = 1;
+      for (int i = 0; i < p->aa; ++i) st[i] = p->pa[p->aa * a + i];
+      for (int j = 0; j < abb; ++j) st[p->aa + j] = B[abb * b + j];
+      for (int i = 0; i < p->aa; ++i)
+        for (int j = 0; j < abb; ++j) shared |= st[i] == st[p->aa + j];
+      if (shared) continue;
+      for (int l = 0; l < ar; ++l) allfixed &= fixed[st[l]];
+      if (allfixed) continue;
+      double x[4][3];
+      for (int l = 0; l < ar; ++l)
+        for (int k = 0; k < 3; ++k) x[l][k] = pts[3 * st[l] + k];
+      const ContactSel sel = kind == K_PT ? classify_pt(x) : kind == K_EE ? classify_ee(x) : classify_pe(x);
+      if (!(contact_dist2_value(sel, x) < dhat)) continue;
+      if (cnt == cap) {
+        cap *= 2;
+        idx = realloc(idx, sizeof(int64_t) * (size_t)(ar * cap));
+      }
+      for (int l = 0; l < ar; ++l) idx[ar * cnt + l] = st[l];
+      ++cnt;
+    }
+  free(p->pairs);
+  p->pairs = idx;
+  p->n = cnt;
+  c->epoch++;
+  free(pts);
+  free(fixed);
+  if (out_n) *out_n = cnt;
   API_END;
 }
 

@@ -95,6 +95,8 @@ _SIGS = {
     "pair_count": [_P, _I32, _PI64],
     "get_pairs": [_P, _I32, _PI64],
     "refresh_pairs": [_P, _I32, _D, _PI32, _PI64],
+    "set_stencil_primitives": [_P, _I32, _I32, _I64, _PI64, _I64, _PI64],
+    "refresh_stencils": [_P, _I32, _D, _PI64],
     "add_stable_neo_hookean": [_P, _I32, _I64, _PI64, _PD, _D, _D, _D, _I32, _PI32],
     "add_point_point_barrier": [_P, _I32, _D, _D, _D, _I32, _PI32],
     "add_repulsive": [_P, _I32, _D, _I32, _PI32],

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-diag-suppress", "177", "-I", str(INCLUDE)]
-SOURCES = ["ys_structure.cu", "ys_assemble.cu", "ys_solver.cu", "ys_dist.cu", "ys_contact.cu", "ys_sell.cu", "ys_capi.cu"]
+SOURCES = ["ys_structure.cu", "ys_assemble.cu", "ys_solver.cu", "ys_dist.cu", "ys_contact.cu", "ys_stencil.cu", "ys_sell.cu", "ys_capi.cu"]
 
 
 def _deps() -> list[Path]:

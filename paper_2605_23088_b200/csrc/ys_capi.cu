@@ -485,6 +485,48 @@ int ys_add_stencil_set(ys_context* c, int32_t uni, int32_t arity, int32_t dynami
   });
 }
 
+int ys_set_stencil_primitives(ys_context* c, int32_t set, int32_t kind, int64_t n_a, const int64_t* prims_a,
+                              int64_t n_b, const int64_t* prims_b) {
+  return guarded(c, [&] {
+    if (set < 0 || set >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown stencil set");
+    PairSet& p = c->pairsets[set];
+    if (kind < 1 || kind > 3) fail(YS_ERR_VALIDATION, "stencil kind must be 1 (PT), 2 (EE) or 3 (PE)");
+    StencilPrims& sp = p.prims;
+    sp.kind = kind == 1 ? K_PT : kind == 2 ? K_EE : K_PE;
+    sp.self = kind == 2;
+    sp.aa = kind == 2 ? 2 : 1;
+    sp.ab = kind == 1 ? 3 : 2;
+    if (sp.aa + sp.ab != p.arity) fail(YS_ERR_DECL, "stencil kind does not match the set's arity");
+    if (n_a < 0 || n_b < 0) fail(YS_ERR_VALIDATION, "negative primitive count");
+    if (sp.self) n_b = 0;
+    int64_t total = 0;
+    for (int32_t d : c->unions[p.uni].children) total += c->domains[d].n;
+    std::vector<int32_t> a(size_t(n_a * sp.aa)), b(size_t(n_b * sp.ab));
+    for (size_t k = 0; k < a.size(); ++k) {
+      if (prims_a[k] < 0 || prims_a[k] >= total) fail(YS_ERR_VALIDATION, "primitive index out of the union");
+      a[k] = int32_t(prims_a[k]);
+    }
+    for (size_t k = 0; k < b.size(); ++k) {
+      if (prims_b[k] < 0 || prims_b[k] >= total) fail(YS_ERR_VALIDATION, "primitive index out of the union");
+      b[k] = int32_t(prims_b[k]);
+    }
+    sp.na = n_a;
+    sp.nb = n_b;
+    sp.a.upload(a, c->stream);
+    sp.b.upload(b, c->stream);
+  });
+}
+
+int ys_refresh_stencils(ys_context* c, int32_t set, double dhat, int64_t* n) {
+  return guarded(c, [&] {
+    require_finalized(*c);
+    if (set < 0 || set >= int32_t(c->pairsets.size())) fail(YS_ERR_DECL, "unknown stencil set");
+    if (!c->pairsets[set].dynamic) fail(YS_ERR_VALIDATION, "resize_dynamic on a static stencil set");
+    if (!(dhat > 0.0)) fail(YS_ERR_VALIDATION, "dhat must be positive");
+    ctx_refresh_stencils(*c, set, dhat, n);
+  });
+}
+
 int ys_add_pair_set(ys_context* c, int32_t uni, int32_t dynamic, int32_t* id) {
   return ys_add_stencil_set(c, uni, 2, dynamic, id);
 }

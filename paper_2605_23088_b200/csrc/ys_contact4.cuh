@@ -318,46 +318,42 @@ __device__ inline void contact_dist2(const ContactSel& s, const double (*x)[3], 
   }
 }
 
-// Value-only squared distance (energy evaluation, line search): the same
-// formulas as contact_dist2 in plain arithmetic.
-__device__ inline double contact_dist2_value(const ContactSel& s, const double (*x)[3]) {
-  auto sub = [](const double* a, const double* b, double* o) {
-    o[0] = a[0] - b[0];
-    o[1] = a[1] - b[1];
-    o[2] = a[2] - b[2];
-  };
-  auto dot = [](const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
-  auto cross = [](const double* a, const double* b, double* o) {
-    o[0] = a[1] * b[2] - a[2] * b[1];
-    o[1] = a[2] * b[0] - a[0] * b[2];
-    o[2] = a[0] * b[1] - a[1] * b[0];
-  };
+// Value-only squared distance (energy evaluation, line search, the candidate
+// test): the same formulas as contact_dist2, explicitly rounded (no FMA
+// contraction), so the candidate test agrees bit for bit with the oracle's.
+__host__ __device__ inline void rn_cross(const double* a, const double* b, double* o) {
+  o[0] = rn_msub(a[1], b[2], a[2], b[1]);
+  o[1] = rn_msub(a[2], b[0], a[0], b[2]);
+  o[2] = rn_msub(a[0], b[1], a[1], b[0]);
+}
+
+__host__ __device__ inline double contact_dist2_value(const ContactSel& s, const double (*x)[3]) {
   double u[3], v[3], w[3], n[3];
   if (s.type == CT_PP) {
-    sub(x[s.b], x[s.a], u);
-    return dot(u, u);
+    rn_sub(x[s.b], x[s.a], u);
+    return rn_dot(u, u);
   }
   if (s.type == CT_PE) {
-    sub(x[s.b], x[s.a], u);
-    sub(x[s.c], x[s.a], v);
-    sub(x[s.c], x[s.b], w);
-    cross(u, v, n);
-    return dot(n, n) / dot(w, w);
+    rn_sub(x[s.b], x[s.a], u);
+    rn_sub(x[s.c], x[s.a], v);
+    rn_sub(x[s.c], x[s.b], w);
+    rn_cross(u, v, n);
+    return rn_dot(n, n) / rn_dot(w, w);
   }
   if (s.type == CT_PT) {
-    sub(x[s.a], x[s.b], u);
-    sub(x[s.c], x[s.b], v);
-    sub(x[s.e], x[s.b], w);
-    cross(v, w, n);
-    const double sp = dot(u, n);
-    return sp * sp / dot(n, n);
+    rn_sub(x[s.a], x[s.b], u);
+    rn_sub(x[s.c], x[s.b], v);
+    rn_sub(x[s.e], x[s.b], w);
+    rn_cross(v, w, n);
+    const double sp = rn_dot(u, n);
+    return rn_mul(sp, sp) / rn_dot(n, n);
   }
-  sub(x[s.b], x[s.a], u);
-  sub(x[s.e], x[s.c], v);
-  sub(x[s.c], x[s.a], w);
-  cross(u, v, n);
-  const double sp = dot(w, n);
-  return sp * sp / dot(n, n);
+  rn_sub(x[s.b], x[s.a], u);
+  rn_sub(x[s.e], x[s.c], v);
+  rn_sub(x[s.c], x[s.a], w);
+  rn_cross(u, v, n);
+  const double sp = rn_dot(w, n);
+  return rn_mul(sp, sp) / rn_dot(n, n);
 }
 
 // Dense symmetric m x m (m <= 12, row-major, full storage) <- V max(L, 0) V^T:

@@ -57,6 +57,16 @@ struct Union {
   std::vector<int64_t> offsets() const;
 };
 
+// Candidate primitives of a contact stencil set (ys_stencil.cu): PT points x
+// triangles, PE points x edges, EE edges x edges (self).
+struct StencilPrims {
+  int kind = 0;  // 0 none, K_PT, K_EE, K_PE
+  bool self = false;
+  int aa = 0, ab = 0;  // points per A / B primitive
+  int64_t na = 0, nb = 0;
+  DevBuf<int32_t> a, b;  // union indices
+};
+
 struct PairSet {
   int32_t uni = -1;
   int32_t arity = 2;  // points per instance: 2 (pairs), 3 (point-edge), 4 (point-triangle, edge-edge)
@@ -64,7 +74,8 @@ struct PairSet {
   int64_t n = 0;
   std::vector<int64_t> h_pairs;
   bool host_stale = false;  // set by the device refresh; get_pairs downloads lazily
-  DevBuf<int32_t> pairs;  // 2n union-global indices
+  DevBuf<int32_t> pairs;  // arity x n union-global indices
+  StencilPrims prims;
 };
 
 // Device scratch of the contact-candidate refresh (ys_contact.cu), reused.
@@ -300,6 +311,7 @@ uint64_t structure_checksum(Context& c, Structure& st, int64_t total_dofs);
 void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed,
                        int64_t* n_pairs);
 void ctx_get_points(Context& c, int domain, double* out);
+void ctx_refresh_stencils(Context& c, int set, double dhat, int64_t* n);  // ys_stencil.cu
 
 // structure pieces reusable by the free-standing BSR path
 void build_structure_from_keys(Context& c, Structure& st, DevBuf<uint64_t>& keys,

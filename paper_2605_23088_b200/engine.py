@@ -230,6 +230,22 @@ class Engine:
         self._arity[pid.value] = int(arity)
         return pid.value
 
+    def set_stencil_primitives(self, stencils: int, kind: str, prims_a, prims_b=None):
+        """Candidate primitives (union indices): kind "pt" (points, triangles),
+        "ee" (edges; self-contact), "pe" (points, edges)."""
+        k = {"pt": 1, "ee": 2, "pe": 3}[kind]
+        a = _i64(prims_a)
+        b = _i64(prims_b if prims_b is not None else [])
+        na = len(a) // (2 if k == 2 else 1)
+        nb = len(b) // (3 if k == 1 else 2)
+        self._c(self.f["set_stencil_primitives"](self.ctx, stencils, k, na, _ip64(a), nb, _ip64(b)))
+
+    def refresh_stencils(self, stencils: int, dhat: float) -> int:
+        """Device contact candidates of a stencil set (resize_dynamic)."""
+        n = C.c_int64()
+        self._c(self.f["refresh_stencils"](self.ctx, stencils, float(dhat), C.byref(n)))
+        return n.value
+
     def set_pairs(self, pairset: int, pairs):
         p = _i64(pairs)
         self._c(self.f["set_pairs"](self.ctx, pairset, len(p) // self._arity.get(pairset, 2), _ip64(p)))

@@ -151,3 +151,82 @@ def test_gpu_matches_oracle_random(kind):
     assert abs(eg - eo) <= 1e-12 * abs(eo)
     assert rel(gg, go) <= 1e-9, rel(gg, go)
     assert rel(hg, ho) <= 1e-9, rel(hg, ho)
+
+
+# ---------------------------------------------------------------------------
+# Contact candidates (ys_refresh_stencils): two free cloth layers over a fixed
+# one — PT (points x triangles), EE self-contact (edges x edges, incident pairs
+# excluded), PE (points x edges) — GPU grid search == oracle all-pairs loop.
+
+def cloth(n, spacing, origin, jitter, rng):
+    y, x = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    v = np.stack([origin[0] + x.ravel() * spacing, np.full(n * n, origin[1]), origin[2] + y.ravel() * spacing], 1)
+    v = v + rng.uniform(-jitter, jitter, v.shape)
+    tris, edges = [], set()
+    for j in range(n - 1):
+        for i in range(n - 1):
+            a, b, c, d = j * n + i, j * n + i + 1, (j + 1) * n + i, (j + 1) * n + i + 1
+            tris += [(a, b, c), (b, d, c)]
+            for e in ((a, b), (a, c), (b, c), (b, d), (c, d)):
+                edges.add(tuple(sorted(e)))
+    return v, np.array(tris), np.array(sorted(edges))
+
+
+def layered_scene(backend, kind, seed=5):
+    rng = np.random.default_rng(seed)
+    n, sp = 9, 0.02
+    v0, t0, e0 = cloth(n, sp, (0.0, 0.0, 0.0), 0.002, rng)
+    v1, t1, e1 = cloth(n, sp, (0.005, 0.012, 0.004), 0.004, rng)
+    vf, tf, ef = cloth(n, sp, (0.0, -0.012, 0.0), 0.0, rng)
+    free = np.concatenate([v0, v1])
+    eng = engine(backend)
+    t = eng.add_target(len(free), 3, free)
+    u = eng.add_point_union([eng.add_points(YS_POINTS_FREE, len(free), t),
+                             eng.add_points(YS_POINTS_FIXED, len(vf), rest=vf)])
+    off1, offf = len(v0), len(free)
+    tris = np.concatenate([t0, t1 + off1, tf + offf])
+    edges = np.concatenate([e0, e1 + off1, ef + offf])
+    pts = np.arange(len(free) + len(vf))
+    arity = 3 if kind == "pe" else 4
+    st = eng.add_stencil_set(u, arity, True)
+    add = {"pt": eng.add_point_triangle_barrier, "ee": eng.add_edge_edge_barrier, "pe": eng.add_point_edge_barrier}
+    add[kind](st, (0.012) ** 2, KAPPA, W)
+    eng.finalize()
+    if kind == "pt":
+        eng.set_stencil_primitives(st, "pt", pts, tris.reshape(-1))
+    elif kind == "ee":
+        eng.set_stencil_primitives(st, "ee", edges.reshape(-1))
+    else:
+        eng.set_stencil_primitives(st, "pe", pts, edges.reshape(-1))
+    return eng, st, tris, edges
+
+
+@pytest.mark.parametrize("kind", ["pt", "ee", "pe"])
+def test_oracle_candidates_exclude_incident_and_fixed(kind):
+    eng, st, tris, edges = layered_scene("oracle", kind)
+    n = eng.refresh_stencils(st, (0.012) ** 2)
+    assert n > 0
+    s = eng.get_pairs(st)
+    assert len(s) == n
+    for row in s[:2000]:
+        assert len(set(row.tolist())) == len(row)  # no shared point
+    nfree = 2 * 81
+    assert np.all((s < nfree).any(axis=1))  # never all-fixed
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["pt", "ee", "pe"])
+def test_gpu_candidates_match_oracle(kind):
+    out = []
+    for b in ("gpu", "oracle"):
+        eng, st, _, _ = layered_scene(b, kind)
+        n = eng.refresh_stencils(st, (0.012) ** 2)
+        out.append((n, eng.get_pairs(st)))
+        eng.refresh_dynamic()
+        eng.assemble(True, True)
+        out[-1] += (eng.gradient().copy(), eng.hessian(1).values.copy(), eng.total_energy())
+    (ng, pg, gg, hg, eg), (no, po, go, ho, eo) = out
+    assert ng == no and ng > 0
+    assert np.array_equal(pg, po)
+    assert rel(gg, go) <= 1e-9 and rel(hg, ho) <= 1e-9
+    assert abs(eg - eo) <= 1e-12 * abs(eo)
