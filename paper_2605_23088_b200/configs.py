@@ -124,6 +124,16 @@ def c4(nx: int = 317, cache_dir: str | None = None) -> dict:
         contact={"enabled": True, "dhat": dh, "kappa": 1e9, "bodies": ["cloth", "sphere"]})
 
 
+def c4_self(nx: int = 64, cache_dir: str | None = None) -> dict:
+    """Extension (not in the reference): C4 at a smaller size with point-triangle
+    and edge-edge self-contact on the cloth (dhat = (0.2 spacing)^2)."""
+    cfg = c4(nx, cache_dir)
+    spacing = 1.0 / (nx - 1)
+    cfg["name"] = "c4_self_contact"
+    cfg["contact"] = dict(cfg["contact"], surface=["cloth"], surface_dhat=(0.2 * spacing) ** 2)
+    return cfg
+
+
 def c5(n=(28, 28, 27), via_f: bool = True) -> dict:
     """Pile of 8 soft blocks (2x2x2), 1,016,064 tets at the default size."""
     bodies, names = [], []
@@ -143,7 +153,7 @@ def c5(n=(28, 28, 27), via_f: bool = True) -> dict:
                 contact={"enabled": True, "dhat": 0.0009, "kappa": 1e9, "bodies": names})
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5, "c4_self": c4_self}
 
 
 def jitter_targets(sim, amplitude: float, seed: int = 7):

@@ -98,6 +98,11 @@ class SimConfig:
     contact_dhat: float = 1e-2
     contact_kappa: float = 1e3
     contact_bodies: list = field(default_factory=list)
+    # extension (not in the reference): point-triangle + edge-edge self-contact
+    # among the triangle surfaces of these bodies, with its own dhat
+    contact_surface: list = field(default_factory=list)
+    contact_surface_dhat: float = 0.0
+    contact_surface_kappa: float = 0.0
     bodies: list = field(default_factory=list)
 
     @staticmethod
@@ -122,6 +127,9 @@ class SimConfig:
             c.contact_dhat = ct.get("dhat", c.contact_dhat)
             c.contact_kappa = ct.get("kappa", c.contact_kappa)
             c.contact_bodies = list(ct.get("bodies", []))
+            c.contact_surface = list(ct.get("surface", []))
+            c.contact_surface_dhat = float(ct.get("surface_dhat", c.contact_dhat))
+            c.contact_surface_kappa = float(ct.get("surface_kappa", c.contact_kappa))
         if not isinstance(j.get("bodies"), list) or not j["bodies"]:
             raise _lib.ValidationError("config needs a non-empty 'bodies' array")
         c.bodies = j["bodies"]
@@ -180,13 +188,14 @@ class Simulation:
         self.dt2 = config.dt * config.dt
         self.contact_pairset = -1
         self.contact_children_fixed: list[int] = []
+        self.surface_sets: list[int] = []  # PT / EE self-contact stencil sets (extension)
         self.energy_labels: list[str] = []
         self._build()
         self.eng.finalize()
         for b in self.bodies:
             if not b.fixed:
                 b.prev_positions = self.body_positions(b).reshape(-1)
-        if self.contact_pairset >= 0 and refresh_pairs:
+        if (self.contact_pairset >= 0 or self.surface_sets) and refresh_pairs:
             self.refresh_dynamic_pairs()
 
     # -------------------------------------------------------------- build
@@ -270,6 +279,7 @@ class Simulation:
                 t = eng.add_target(n, 3, v)
                 body.targets = [t]
                 body.domain = eng.add_points(YS_POINTS_FREE, n, t)
+                body.tris = np.asarray(tris, dtype=np.int64).reshape(-1, 3)
                 hg = hinges(tris)
                 if len(hg):
                     eng.add_bending(t, hg.reshape(-1), v, float(bj.get("bending_stiffness", 0.055)), self.dt2)
@@ -307,15 +317,53 @@ class Simulation:
             self.contact_pairset = eng.add_pair_set(uni, True)
             self.contact_children_fixed = fixed
             eng.add_point_point_barrier(self.contact_pairset, cfg.contact_dhat, cfg.contact_kappa, self.dt2)
+        if cfg.contact_surface:
+            self._build_surface_contact()
+
+    def _build_surface_contact(self):
+        """Extension (not in the reference): point-triangle and edge-edge
+        self-contact among the triangle surfaces of `contact.surface` bodies
+        (ys_contact4.cuh / ys_stencil.cu), the point-point barrier's b(d) on
+        the squared distance, dhat = `contact.surface_dhat`, kappa =
+        `contact.surface_kappa` (default: the point-point kappa)."""
+        eng, cfg = self.eng, self.config
+        doms, tris, off = [], [], 0
+        for name in cfg.contact_surface:
+            b = next((b for b in self.bodies if b.name == name), None)
+            if b is None or getattr(b, "tris", None) is None:
+                raise _lib.ValidationError(f"surface contact body '{name}' is not a free triangle surface")
+            doms.append(b.domain)
+            tris.append(b.tris + off)
+            off += b.n
+        tri = np.concatenate(tris)
+        e = np.sort(np.concatenate([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [0, 2]]]), axis=1)
+        edges = np.unique(e, axis=0)
+        uni = eng.add_point_union(doms)
+        pt = eng.add_stencil_set(uni, 4, True)
+        ee = eng.add_stencil_set(uni, 4, True)
+        eng.add_point_triangle_barrier(pt, cfg.contact_surface_dhat, cfg.contact_surface_kappa, self.dt2)
+        eng.add_edge_edge_barrier(ee, cfg.contact_surface_dhat, cfg.contact_surface_kappa, self.dt2)
+        self._surface_prims = (pt, np.arange(off), tri.reshape(-1), ee, edges.reshape(-1))
+        self.surface_sets = [pt, ee]
 
     # -------------------------------------------------------------- driver
     def body_positions(self, b: Body) -> np.ndarray:
         return self.eng.get_points(b.domain, b.n)
 
     def refresh_dynamic_pairs(self) -> int:
-        """Simulation::refresh_dynamic_pairs (sim.cpp:456-484), on the engine's device."""
+        """Simulation::refresh_dynamic_pairs (sim.cpp:456-484), on the engine's device
+        (plus the PT / EE self-contact stencils of the surface extension)."""
+        n = 0
+        if self.surface_sets:
+            pt, pts, tri, ee, edges = self._surface_prims
+            if not getattr(self, "_surface_prims_set", False):
+                self.eng.set_stencil_primitives(pt, "pt", pts, tri)
+                self.eng.set_stencil_primitives(ee, "ee", edges)
+                self._surface_prims_set = True
+            for st in self.surface_sets:
+                self.eng.refresh_stencils(st, self.config.contact_surface_dhat)
         if self.contact_pairset < 0:
-            return 0
+            return n
         return self.eng.refresh_pairs(self.contact_pairset, self.config.contact_dhat, self.contact_children_fixed)
 
     def pair_count(self) -> int:
@@ -376,7 +424,7 @@ class Simulation:
             rep.energy = e_new
             rep.energy_nonincreasing = rep.energy_nonincreasing and e_new <= e0
             rep.last_step_norm = step
-            if self.contact_pairset >= 0:
+            if self.contact_pairset >= 0 or self.surface_sets:
                 self.refresh_dynamic_pairs()
             if rep.last_step_norm / cfg.dt < cfg.newton_tol:
                 rep.converged = True
@@ -385,7 +433,7 @@ class Simulation:
 
     def step(self) -> NewtonReport:
         self.begin_frame()
-        if self.contact_pairset >= 0:
+        if self.contact_pairset >= 0 or self.surface_sets:
             self.refresh_dynamic_pairs()
         rep = self.newton_solve()
         self.end_frame()

@@ -19,3 +19,4 @@ for _ in range(steps):
     sim.eng.bump_dynamic_epoch()
     st = sim.eng.minimize_step(cfg.pcg_tol, -1, want_dx=False)
 print(name, "pcg_iterations", st.pcg_iterations, "path", sim.eng.pcg_path())
+sim.eng.close()  # destroy the context: compute-sanitizer --leak-check sees every allocation freed
