@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--via-f", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--state", default="rollout", choices=["rollout", "jitter"])
+    p.add_argument("--frames", type=int, default=None, help="rollout frames (default: the config's, 25 for C5)")
     return p.parse_args()
 
 
@@ -80,9 +82,27 @@ def jitter_amplitude(name: str) -> float:
     return 0.1 * (0.025 if name == "c1" else 0.02 if name == "c3" else 0.01)
 
 
-def prepare(name: str, via_f: bool, backend: str, device: int = 0):
-    """Scene + prepared state: seeded jitter of the soft vertices, x_tilde of
-    frame 1 (begin_frame), contact pairs of that state."""
+def prepare(name: str, via_f: bool, backend: str, device: int = 0, state: str = "rollout", frames: int | None = None):
+    """Scene + prepared state ("time from a prepared state").
+
+    state "rollout" (default): the scene's first `frames` frames (config
+    `frames`, 25 for C5 as in test_acceptance.cpp:460) simulated on the B200
+    library — Newton + line search + contact refresh per iteration, bitwise
+    deterministic — then begin_frame of the next frame and its contact pairs.
+    The oracle side ("oracle") takes that state over (positions, velocities,
+    then its own begin_frame) and refreshes its pairs with the reference's
+    all-pairs loop: the O(n^2) refresh and ~8 s Newton iterations make a CPU
+    rollout of C5 impractical (CPU baseline).
+    state "jitter" (round 1): seeded jitter of the soft vertices at rest."""
+    if state == "jitter":
+        return _jitter_state(name, via_f, backend, device)
+    gsim = rollout(name, via_f, device, frames)
+    if backend == "gpu":
+        return gsim
+    return oracle_from(gsim, name, via_f)
+
+
+def _jitter_state(name, via_f, backend, device):
     from paper_2605_23088_b200 import configs
     from paper_2605_23088_b200.scene import SimConfig
     cfg = SimConfig.from_dict(scene_config(name, via_f))
@@ -90,6 +110,43 @@ def prepare(name: str, via_f: bool, backend: str, device: int = 0):
     configs.jitter_targets(sim, jitter_amplitude(name))
     sim.begin_frame()
     sim.refresh_dynamic_pairs()
+    return sim
+
+
+def rollout(name: str, via_f: bool, device: int = 0, frames: int | None = None):
+    from paper_2605_23088_b200.scene import SimConfig
+    cfg = SimConfig.from_dict(scene_config(name, via_f))
+    sim = simulation(cfg, "gpu", device=device)
+    sim.prepared_frames = cfg.frames if frames is None else frames
+    sim.rollout_newton = 0
+    for _ in range(sim.prepared_frames):
+        sim.rollout_newton += sim.step().iterations
+    sim.begin_frame()
+    sim.refresh_dynamic_pairs()
+    return sim
+
+
+def oracle_from(src, name: str, via_f: bool, pairs=None):
+    """An oracle Simulation in the state of `src` (a prepared GPU Simulation):
+    target values and body velocities copied, begin_frame recomputed on the
+    host (the same numpy arithmetic: identical x_tilde), contact pairs from the
+    reference's all-pairs loop or, when given, the GPU's (bit-identical list,
+    tests/test_gpu_large.py)."""
+    from paper_2605_23088_b200.scene import SimConfig
+    cfg = SimConfig.from_dict(scene_config(name, via_f))
+    sim = simulation(cfg, "oracle", refresh_pairs=False)
+    for bs, bd in zip(src.bodies, sim.bodies):
+        for t in bs.targets:
+            sim.eng.set_target_values(t, src.eng.get_target_values(t))
+        if bs.velocity is not None:
+            bd.velocity = np.array(bs.velocity, copy=True)
+    sim.begin_frame()
+    if sim.contact_pairset >= 0:
+        if pairs is None:
+            sim.refresh_dynamic_pairs()
+        else:
+            sim.eng.set_pairs(sim.contact_pairset, pairs)
+    sim.prepared_frames = getattr(src, "prepared_frames", 0)
     return sim
 
 
@@ -147,27 +204,6 @@ def traffic_from_profiles(scene: str, key: str):
         return None
 
 
-def oracle_state(name: str, via_f: bool, pairs=None):
-    """The bench's prepared state on the oracle port (the reference's algorithm
-    restated in C, pinned to the reference itself: tests/test_golden.py,
-    tests/test_reference.py): the same config, jitter and begin_frame; the
-    contact pairs from the reference's all-pairs loop, or — for the GPU arm's
-    bounded sample — the GPU's list, which is bit-identical
-    (tests/test_gpu_large.py) and spares the O(n^2) refresh."""
-    from paper_2605_23088_b200 import configs
-    from paper_2605_23088_b200.scene import SimConfig
-    cfg = SimConfig.from_dict(scene_config(name, via_f))
-    sim = simulation(cfg, "oracle", refresh_pairs=False)
-    configs.jitter_targets(sim, jitter_amplitude(name))
-    sim.begin_frame()
-    if sim.contact_pairset >= 0:
-        if pairs is None:
-            sim.refresh_dynamic_pairs()
-        else:
-            sim.eng.set_pairs(sim.contact_pairset, pairs)
-    return sim
-
-
 def cpu_threads() -> int:
     """All host threads, as the reference configured with "threads" = nproc:
     instance evaluation (parallel_for, assembly.cpp:334-336) and the sharded
@@ -188,11 +224,12 @@ def cpu_step(sim):
     return 1e3 * (time.perf_counter() - t0), st
 
 
-def cpu_sample(name: str, via_f: bool, pairs):
+def cpu_sample(gsim, name: str, via_f: bool):
     """Bounded CPU sample for the GPU arm: ONE full-scene Newton iteration of the
-    same workload on the oracle port, on all host threads (~10-20 s at C5)."""
+    same workload (the GPU arm's prepared state, its bit-identical pair list) on
+    the oracle port, on all host threads (~10-20 s at C5)."""
     threads = cpu_threads()
-    sim = oracle_state(name, via_f, pairs)
+    sim = oracle_from(gsim, name, via_f, _read_pairs(gsim) if gsim.contact_pairset >= 0 else None)
     ms, st = cpu_step(sim)
     return {"value": ms, "unit": "ms", "cores": threads, "kind": "port",
             "sample": (f"{name}: one full Newton iteration (minimize_step: dynamic rebuild, instance evaluation on "
@@ -212,7 +249,14 @@ def run_reference(args):
         return
     threads = cpu_threads()
     t0 = time.perf_counter()
-    sim = oracle_state(args.config, bool(args.via_f))
+    gsim = rollout(args.config, bool(args.via_f), 0, args.frames) if args.state == "rollout" else None
+    prep_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    if gsim is not None:
+        sim = oracle_from(gsim, args.config, bool(args.via_f))
+        gsim.eng.close()
+    else:
+        sim = _jitter_state(args.config, bool(args.via_f), "oracle", 0)
     setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
         cpu_step(sim)
@@ -225,11 +269,14 @@ def run_reference(args):
     cb = {"value": v, "unit": "ms", "cores": threads, "kind": "port",
           "sample": (f"{args.config}: the full scene, {args.warmup} untimed + {args.steps} timed Newton iterations "
                      f"(minimize_step) on {threads} host threads; PCG iterations {int(np.median(iters))}; "
-                     f"setup (scene build + the reference's all-pairs contact refresh) {setup_s:.1f} s untimed")}
+                     f"setup (scene build + the reference's all-pairs contact refresh) {setup_s:.1f} s untimed; "
+                     + (f"state: {args.frames if args.frames is not None else 'config'} frames rolled out on the B200 "
+                        f"library ({prep_s:.1f} s untimed, deterministic) and taken over by the port"
+                        if gsim is not None else "state: seeded jitter at rest"))}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args.config), "scene": args.config, "dofs": int(sim.eng.s),
+            "config": {"workload": workload(args.config, args.state, sim), "scene": args.config, "dofs": int(sim.eng.s),
                        "contact_pairs": int(sim.pair_count()), "pcg_iterations": int(np.median(iters)),
                        "pcg_iterations_per_step": [int(i) for i in iters], "ms_per_step_min": min(vals),
                        "ms_per_step_max": max(vals), "nh_via_deformation_gradient": bool(args.via_f),
@@ -238,9 +285,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload(name: str) -> str:
+def workload(name: str, state: str = "rollout", sim=None) -> str:
+    if state == "jitter":
+        where = "from a jittered rest state"
+    else:
+        where = f"from the prepared state after {getattr(sim, 'prepared_frames', '?')} simulated frames"
     return (f"{name}: one Newton iteration (dynamic rebuild + eval + assembly + block-Jacobi + PCG to pcg_tol) "
-            f"from a jittered rest state")
+            + where)
 
 
 def spawn_ranks(args):
@@ -276,7 +327,9 @@ def main():
     torch.cuda.set_device(local)
 
     from paper_2605_23088_b200 import _lib
-    sim = prepare(args.config, bool(args.via_f), "gpu", local)
+    t_prep = time.perf_counter()
+    sim = prepare(args.config, bool(args.via_f), "gpu", local, args.state, args.frames)
+    t_prep = time.perf_counter() - t_prep
     eng = sim.eng
     if world > 1:
         from paper_2605_23088_b200 import dist as ysdist
@@ -372,7 +425,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_sample(args.config, bool(args.via_f), _read_pairs(sim) if sim.contact_pairset >= 0 else None)
+            cpu = cpu_sample(sim, args.config, bool(args.via_f))
         except Exception as exc:  # reported, not fatal
             cpu = {"value": None, "unit": "ms", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -384,10 +437,12 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload(args.config),
+        "config": {"workload": workload(args.config, args.state, sim),
                    "scene": args.config, "tets": stats_tets, "dofs": int(eng.s),
                    "contact_pairs": int(sim.pair_count()), "pcg_iterations": int(np.median(iters)),
                    "nh_via_deformation_gradient": bool(args.via_f),
+                   "prepared_frames": getattr(sim, "prepared_frames", 0),
+                   "prepare_s": round(t_prep, 2),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
                    "parallelism": f"pcg-rows{world} (eval/assembly replicated)" if world > 1 else "single"},
         "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else

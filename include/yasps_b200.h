@@ -287,7 +287,9 @@ int ys_dist_info(ys_context* ctx, int32_t* rank, int32_t* nranks, int64_t* bound
  * [12..15] its sub-phase clocks (ms must hold 16 doubles).
  * counts[0] = kernel launches, counts[1] = indefinite 9x9 projections of the
  * last assembly, counts[2] = uniform-3x3 PCG path of the last solve (1 sliced-ELL
- * copy, 2 row gather from upper storage; 0 other).
+ * copy, 2 row gather from upper storage; 0 other), counts[3] = of the
+ * indefinite projections, those done by the Jacobi fallback (counts must hold
+ * 4 values).
  * ------------------------------------------------------------------------ */
 int ys_set_profiling(ys_context* ctx, int32_t enabled);
 int ys_stage_times(ys_context* ctx, double* ms, int64_t* counts);
@@ -297,9 +299,13 @@ int ys_bump_dynamic_epoch(ys_context* ctx);
 /* The cudaStream_t every kernel of the context is launched on (for CUDA-event
  * timing by the caller). */
 int ys_stream(ys_context* ctx, void** stream);
-/* Execution options (no effect on results): "overlap" (default 1) evaluates the
- * static energies on side streams while minimize_step rebuilds the dynamic
- * group; 0 runs the stages sequentially (bitwise the same step). */
+/* Execution options: "overlap" (default 1) evaluates the static energies on
+ * side streams while minimize_step rebuilds the dynamic group; 0 runs the
+ * stages sequentially (bitwise the same step).  "eval_evd" (default 1) projects
+ * the indefinite 9x9 element Hessians by the clamped-eigenpair path
+ * (tridiagonal QL + inverse iteration, verified; failures go to the Jacobi
+ * EVD); 0 sends every element through the Jacobi EVD (both within 1e-12 of
+ * the exact projection). */
 int ys_set_option(ys_context* ctx, const char* name, int64_t value);
 /* Times one kernel class alone: reps launches bracketed by CUDA events on the
  * context stream.  which: 0 = SpMV row gather from upper storage (static +

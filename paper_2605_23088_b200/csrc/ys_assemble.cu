@@ -186,7 +186,74 @@ struct StencilBatch {
   double* hc[kStencilBatch];
   const unsigned int* count[kStencilBatch];
   int64_t base[kStencilBatch];  // first list / M slot of each energy
+  unsigned int* fbcount[kStencilBatch];  // elements handed to the Jacobi path, per energy
+  int32_t* fblist[kStencilBatch];        // their local list positions (k - first of the energy)
 };
+
+// Pass B, main path: the clamped-eigenpair projection (psd_project9_tri,
+// ~5k FP64 operations, registers + 552 B of shared memory per thread); an
+// element whose verification fails goes to its energy's fallback list.
+template <int KIND>
+__global__ void __launch_bounds__(kProjStride) k_eval_stencil_b_tri(const __grid_constant__ StencilBatch B,
+                                                                    const int32_t* __restrict__ list,
+                                                                    const double* __restrict__ mbuf) {
+  extern __shared__ double sm_proj[];
+  unsigned pre[kStencilBatch + 1];
+  pre[0] = 0;
+#pragma unroll
+  for (int j = 0; j < kStencilBatch; ++j) pre[j + 1] = pre[j] + (j < B.n ? *B.count[j] : 0u);
+  const unsigned total = pre[kStencilBatch];
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    int j = 0;
+#pragma unroll
+    for (int q = 1; q < kStencilBatch; ++q) j += k >= pre[q] ? 1 : 0;
+    const EnergyDev& E = B.e[j];
+    const int64_t slot = B.base[j] + (k - pre[j]);
+    double m[45];
+    if (!psd_project9_tri(mbuf + 45 * slot, m, sm_proj + threadIdx.x)) {
+      const unsigned f = atomicAdd(B.fbcount[j], 1u);
+      B.fblist[j][f] = int32_t(k - pre[j]);
+      continue;
+    }
+    const int64_t i = list[slot];
+    const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
+    const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
+    const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
+    const VertexBlockWriter wr{B.hc[j] + inst_hoff(E, i), vertex_pair_swaps(gs)};
+    expand_vertex_blocks(m, full, wr);
+  }
+}
+
+// Pass B, fallback: the cyclic Jacobi EVD (psd_project9) for the elements the
+// main path handed over (all of them with ys_set_option("eval_evd", 0)).
+template <int KIND>
+__global__ void __launch_bounds__(128) k_eval_stencil_b_fallback(const __grid_constant__ StencilBatch B,
+                                                                 const int32_t* __restrict__ list,
+                                                                 const double* __restrict__ mbuf) {
+  unsigned pre[kStencilBatch + 1];
+  pre[0] = 0;
+#pragma unroll
+  for (int j = 0; j < kStencilBatch; ++j) pre[j + 1] = pre[j] + (j < B.n ? *B.fbcount[j] : 0u);
+  const unsigned total = pre[kStencilBatch];
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
+    int j = 0;
+#pragma unroll
+    for (int q = 1; q < kStencilBatch; ++q) j += k >= pre[q] ? 1 : 0;
+    const EnergyDev& E = B.e[j];
+    const int64_t slot = B.base[j] + B.fblist[j][k - pre[j]];
+    const int64_t i = list[slot];
+    double m[45];
+    const double* src = mbuf + 45 * slot;
+#pragma unroll
+    for (int q = 0; q < 45; ++q) m[q] = src[q];
+    psd_project9(m);
+    const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
+    const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
+    const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
+    const VertexBlockWriter wr{B.hc[j] + inst_hoff(E, i), vertex_pair_swaps(gs)};
+    expand_vertex_blocks(m, full, wr);
+  }
+}
 
 template <int KIND>
 __global__ void __launch_bounds__(128) k_eval_stencil_b_batch(const __grid_constant__ StencilBatch B,
@@ -880,7 +947,9 @@ static void record(Context& c, int idx) {
 // (two streams share the static energies; the caller zeroes the counters).
 void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStream_t s, int part, bool zero_counts) {
   if (!s) s = c.stream;
-  c.evd_count.resize(std::max(c.evd_count.n, c.energies.size()));
+  // evd_count: [0, n) indefinite elements per energy, [n, 2n) of those the
+  // Jacobi fallback projects
+  c.evd_count.resize(std::max(c.evd_count.n, 2 * c.energies.size()));
   if (only != 1 && zero_counts) c.evd_count.zero(s);
   // every stencil energy gets its own compacted-list / M range, so pass B can
   // run once for all energies of a kind after their pass A
@@ -895,6 +964,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
   }
   c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * evd_total)));
   c.evd_list.resize(std::max(c.evd_list.n, size_t(evd_total)));
+  c.evd_fblist.resize(std::max(c.evd_fblist.n, size_t(evd_total)));
   const bool pass_b = with_hessian && project;
   // pass B (Jacobi EVD of the indefinite elements) runs right after each
   // energy's pass A, while its M buffer (360 B per indefinite element) sits in
@@ -916,13 +986,38 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
       B.hc[j] = c.S[e.dynamic ? 1 : 0].hcontrib.p;
       B.count[j] = c.evd_count.p + pending[j];
       B.base[j] = evd_base[pending[j]];
+      B.fbcount[j] = c.evd_count.p + c.energies.size() + pending[j];
+      B.fblist[j] = c.evd_fblist.p + evd_base[pending[j]];
     }
-    if (pending_kind == 0)
-      k_eval_stencil_b_batch<0><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
-    else
-      k_eval_stencil_b_batch<1><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
-    YS_LAUNCH_CHECK();
-    ++c.launches;
+    if (c.evd_mode == 0) {
+      // every indefinite element through the Jacobi EVD
+      if (pending_kind == 0)
+        k_eval_stencil_b_batch<0><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+      else
+        k_eval_stencil_b_batch<1><<<gb, 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+      YS_LAUNCH_CHECK();
+      ++c.launches;
+    } else {
+      static bool attr = false;
+      const size_t smem = size_t(kProjSlots) * kProjStride * sizeof(double);
+      if (!attr) {
+        YS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_eval_stencil_b_tri<0>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        YS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_eval_stencil_b_tri<1>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+      }
+      const unsigned gt = unsigned(sm_count() * 3);
+      if (pending_kind == 0) {
+        k_eval_stencil_b_tri<0><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p);
+        k_eval_stencil_b_fallback<0><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+      } else {
+        k_eval_stencil_b_tri<1><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p);
+        k_eval_stencil_b_fallback<1><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
+      }
+      YS_LAUNCH_CHECK();
+      c.launches += 2;
+    }
     pending.clear();
     pending_n = 0;
   };

@@ -884,7 +884,7 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
       }
       // the static energies split over two streams (even / odd index): one
       // energy's pass-B tail overlaps the other stream's work
-      c->evd_count.resize(std::max(c->evd_count.n, c->energies.size()));
+      c->evd_count.resize(std::max(c->evd_count.n, 2 * c->energies.size()));
       c->evd_count.zero(c->stream);
       YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
       YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
@@ -1089,13 +1089,15 @@ int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
     for (int k = 0; k < 8; ++k) ms[8 + k] = c->pcg_phase_ms[k];
     if (counts) {
       counts[0] = c->launches;
-      int64_t evd = 0;
+      int64_t evd = 0, fb = 0;
       if (c->evd_count.n) {
         std::vector<unsigned int> h = c->evd_count.to_host(c->stream);
-        for (unsigned v : h) evd += v;
+        const size_t ne = c->energies.size();
+        for (size_t k = 0; k < h.size(); ++k) (k < ne ? evd : fb) += k < 2 * ne ? h[k] : 0;
       }
-      counts[1] = evd;  // indefinite 9x9 projections (EVD pass) in the last assembly
+      counts[1] = evd;  // indefinite 9x9 projections (pass B) in the last assembly
       counts[2] = c->pcg_path;
+      counts[3] = fb;   // of those, projected by the Jacobi fallback
     }
   });
 }
@@ -1290,7 +1292,10 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
   return guarded(c, [&] {
     const std::string n = name ? name : "";
     if (n == "overlap") c->overlap = value != 0;
-    else fail(YS_ERR_VALIDATION, "unknown option '" + n + "'");
+    else if (n == "eval_evd") {
+      if (value != 0 && value != 1) fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi) or 1 (clamped eigenpairs)");
+      c->evd_mode = int(value);
+    } else fail(YS_ERR_VALIDATION, "unknown option '" + n + "'");
   });
 }
 

@@ -261,12 +261,14 @@ struct Context {
   // two-pass projection of 9x9 edge-space Hessians (SNH, bending)
   DevBuf<double> evd_m;          // pending M (45 per entry)
   DevBuf<int32_t> evd_list;      // pending element ids
-  DevBuf<unsigned int> evd_count;  // one counter per energy
+  DevBuf<unsigned int> evd_count;  // per energy: indefinite elements, then Jacobi-fallback elements
+  DevBuf<int32_t> evd_fblist;      // fallback elements (local list positions)
   int64_t evd_last = 0;          // indefinite elements of the last assembly (diagnostics)
 
   // profiling
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
+  int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only
   double stage_ms[8] = {0};
   double pcg_phase_ms[8] = {0};
   int64_t launches = 0;

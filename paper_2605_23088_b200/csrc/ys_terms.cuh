@@ -160,6 +160,367 @@ __device__ __forceinline__ int psd_project9(double* a) {
 }
 
 // ---------------------------------------------------------------------------
+// Clamped-eigenpair projection of a packed 9x9 M (pass B's main path):
+//   1. Householder tridiagonalization T = Q^T M Q, Q = H_0 ... H_6 (the
+//      reflectors go to shared memory: slots [0, 35) v_k, [35, 42) beta_k);
+//   2. all eigenvalues of T by implicit QL (Wilkinson-type shift), the sweep
+//      over the unreduced block written as a static loop over i with a
+//      predicate l <= i < m (registers only, small code);
+//   3. the number of eigenvalues below -tau0 (tau0 = 1e-13 |M|_F; those in
+//      (-tau0, 0] are left unclamped, an error <= tau0) cross-checked with a
+//      Sturm count of T at -tau0;
+//   4. eigenvectors only for the clamped side — the k <= 4 negative
+//      eigenvalues (P = M - sum lam x x^T) or else the <= 4 others
+//      (P = sum max(lam, 0) x x^T) — by inverse iteration on T (pivoted
+//      tridiagonal LU, 2 solves; members of a cluster Gram-Schmidt
+//      orthogonalized against the earlier ones), kept in the T basis in
+//      shared-memory slots [42, 78) and back-transformed with the reflectors
+//      when P is formed;
+//   5. verification: every used pair's residual |T y - lam y| <= 1e-12 |M|_F
+//      and used vectors orthogonal to 1e-12.  Then |P - Proj(M)| is bounded
+//      by ~1e-12 |M|_F: a contaminating eigenvector of the same sign is used
+//      too (orthogonality), one of the other sign is at least |lam| away, so
+//      the residual bounds the error (plus the Householder backward error,
+//      ~1e-15 |M|_F).
+// Returns false when a check fails or QL does not converge: the caller hands
+// the element to the Jacobi path (psd_project9).
+// Measured on C5 tets (tools/evd_proto3.py, the same algorithm in numpy):
+// 100 % accepted at the rolled-out and the jittered state, max |P - eigh| /
+// max|M| = 3.7e-15.  ~5k FP64 operations against ~19k for the Jacobi EVD.
+// sm: this thread's slot 0 in a [69][kProjStride] shared array.
+constexpr int kProjStride = 128;
+
+// Reload of M at the end of the projection: a volatile load, so the compiler
+// neither keeps the first load's 45 values live across the QL (CSE of the
+// read-only loads) nor hoists the reload (90 registers either way).
+__device__ __forceinline__ double ld_reload(const double* p) {
+  double v;
+  asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+constexpr int kProjSlots = 78;
+
+__device__ __forceinline__ int refl_off(int k) { return k * 8 - (k * (k - 1)) / 2; }  // sum_{i<k} (8 - i)
+
+__device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc, double* P, double* sm) {
+  auto S = [&](int slot) -> double& { return sm[slot * kProjStride]; };
+  double a[45];
+  double n2 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 45; ++q) a[q] = msrc[q];
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) n2 += (i == j ? 1.0 : 2.0) * a[pk9(i, j)] * a[pk9(i, j)];
+  const double nrm = sqrt(n2);
+  // ---- 1. tridiagonalization
+  double e[8];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const int m = 8 - k;
+    double x0 = a[pk9(k + 1, k)];
+    double sig = 0.0;
+#pragma unroll
+    for (int i = 1; i < m; ++i) sig += a[pk9(k + 1 + i, k)] * a[pk9(k + 1 + i, k)];
+    const double nx = sqrt(x0 * x0 + sig);
+    double beta = 0.0, alpha = 0.0;
+    if (nx != 0.0) {
+      alpha = x0 >= 0.0 ? -nx : nx;
+      beta = 1.0 / (nx * nx - x0 * alpha);
+    }
+    double v[8];
+    v[0] = x0 - alpha;
+#pragma unroll
+    for (int i = 1; i < m; ++i) v[i] = a[pk9(k + 1 + i, k)];
+    // p = beta S v, K = beta/2 p.v, w = p - K v; S -= v w^T + w v^T
+    double p[8];
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < m; ++j) acc += a[pk9(k + 1 + i, k + 1 + j)] * v[j];
+      p[i] = beta * acc;
+    }
+    double pv = 0.0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) pv += p[i] * v[i];
+    const double K = 0.5 * beta * pv;
+#pragma unroll
+    for (int i = 0; i < m; ++i) p[i] -= K * v[i];
+#pragma unroll
+    for (int i = 0; i < m; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) a[pk9(k + 1 + i, k + 1 + j)] -= v[i] * p[j] + p[i] * v[j];
+    e[k] = nx != 0.0 ? alpha : 0.0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) S(refl_off(k) + i) = v[i];
+    S(35 + k) = beta;
+  }
+  e[7] = a[pk9(8, 7)];
+  double d[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) d[i] = a[pk9(i, i)];
+  // ---- 2. eigenvalues (implicit QL on copies).  One loop iteration = one QL
+  // sweep of this lane's current unreduced block [l, m]; lanes deflate
+  // independently (the warp runs max over its lanes of the total sweep count,
+  // not the per-level maxima), and the static 8-step sweep stops as soon as
+  // every lane of the warp is below its block.
+  double lam[9], ee[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    lam[i] = d[i];
+    ee[i] = i < 8 ? e[i] : 0.0;
+  }
+  {
+    int l = 0;
+    for (int sweep = 0;; ++sweep) {
+      // deflate: l = first index whose coupling to the next is not negligible
+      int m = 8;
+      bool found_l = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double dd = fabs(lam[i]) + fabs(lam[i + 1]);
+        const bool neg = fabs(ee[i]) + dd == dd;
+        if (!found_l && i >= l && !neg) {
+          l = i;
+          found_l = true;
+        }
+        if (found_l && i > l - 1 && neg && m == 8 && i >= l) m = i;
+      }
+      if (!found_l) l = 8;
+      const bool active = l < 8;
+      if (!__any_sync(__activemask(), active)) break;
+      if (sweep == 120) return false;
+      if (active) {
+        double dl = 0.0, dl1 = 0.0, el = 0.0, dm = 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          if (i == l) {
+            dl = lam[i];
+            el = ee[i];
+          }
+          if (i == l + 1) dl1 = lam[i];
+          if (i == m) dm = lam[i];
+        }
+        double g = (dl1 - dl) / (2.0 * el);
+        double r = hypot(g, 1.0);
+        g = dm - dl + el / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, pp = 0.0;
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          if (i < m && i >= l) {
+            const double f = s * ee[i], b = c * ee[i];
+            const double r2 = f * f + g * g;
+            if (r2 == 0.0) {
+              ee[i + 1] = 0.0;
+              s = 0.0;
+              c = 1.0;
+            } else {
+              const double ir = rsqrt(r2);
+              ee[i + 1] = r2 * ir;
+              s = f * ir;
+              c = g * ir;
+            }
+            g = lam[i + 1] - pp;
+            r = (lam[i] - g) * s + 2.0 * c * b;
+            pp = s * r;
+            lam[i + 1] = g + pp;
+            g = c * r - b;
+          }
+          if (i > 0 && !__any_sync(__activemask(), i - 1 >= l)) break;
+        }
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          if (i == l) {
+            lam[i] -= pp;
+            ee[i] = g;
+          }
+          if (i == m) ee[i] = 0.0;
+        }
+      }
+    }
+  }
+  // sort ascending (odd-even transposition)
+#pragma unroll
+  for (int rnd = 0; rnd < 9; ++rnd)
+#pragma unroll
+    for (int i = rnd & 1; i + 1 < 9; i += 2) {
+      const double lo = fmin(lam[i], lam[i + 1]), hi = fmax(lam[i], lam[i + 1]);
+      lam[i] = lo;
+      lam[i + 1] = hi;
+    }
+  // eigenvalues in (-tau0, 0] count as zero: leaving them unclamped changes P
+  // by at most tau0 = 1e-13 |M|_F (and their sign is not resolved anyway)
+  const double tau0 = 1e-13 * nrm;
+  int kneg = 0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) kneg += lam[i] < -tau0;
+  // ---- 3. Sturm count of T at -tau0 must agree
+  double tn = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) tn = fmax(tn, fabs(d[i]) + (i < 8 ? fabs(e[i]) : 0.0) + (i > 0 ? fabs(e[i - 1]) : 0.0));
+  const double pivmin = 1e-300 + 2.2e-19 * tn;
+  {
+    int cnt = 0;
+    double q = d[0] + tau0;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+      q = d[i] + tau0 - e[i - 1] * e[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0.0;
+    }
+    if (cnt != kneg) return false;
+  }
+  if (kneg == 0) {
+#pragma unroll
+    for (int q = 0; q < 45; ++q) P[q] = ld_reload(msrc + q);
+    return true;
+  }
+  // clamped side: the kneg <= 4 negative eigenvalues, else the <= 4 others
+  const bool negside = kneg <= 4;
+  const int nuse = negside ? kneg : 9 - kneg;
+  // ---- 4. eigenvectors of T for the used eigenvalues (T basis, smem slots
+  // [42, 78)); members of a cluster (|lam_u - lam_w| <= 1e-3 |T|) are
+  // Gram-Schmidt orthogonalized against the earlier ones after every solve
+  double lu[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+  for (int u = 0; u < nuse; ++u) {
+    const int sel = negside ? u : kneg + u;
+    double lj = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if (i == sel) lj = lam[i];
+    // pivoted LU of T - lj I (LAPACK dgttrf layout)
+    double D[9], DL[8], DU[8], DU2[7], rD[9];
+    bool piv[8];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) D[i] = d[i] - lj;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      DL[i] = e[i];
+      DU[i] = e[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 7; ++i) DU2[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      piv[i] = !(fabs(D[i]) >= fabs(DL[i]));
+      if (!piv[i]) {
+        if (D[i] == 0.0) D[i] = pivmin;
+        rD[i] = 1.0 / D[i];
+        const double fact = DL[i] * rD[i];
+        DL[i] = fact;
+        D[i + 1] -= fact * DU[i];
+      } else {
+        rD[i] = 1.0 / DL[i];
+        const double fact = D[i] * rD[i];
+        D[i] = DL[i];
+        DL[i] = fact;
+        const double temp = DU[i];
+        DU[i] = D[i + 1];
+        D[i + 1] = temp - fact * D[i + 1];
+        if (i < 7) {
+          DU2[i] = DU[i + 1];
+          DU[i + 1] = -fact * DU[i + 1];
+        }
+      }
+    }
+    if (D[8] == 0.0) D[8] = pivmin;
+    rD[8] = 1.0 / D[8];
+    double y[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) y[i] = 1.0 / 3.0 + ((i + 2 * u) % 9 == 0 ? 0.25 : 0.0);
+#pragma unroll
+    for (int itr = 0; itr < 2; ++itr) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (piv[i]) {
+          const double t = y[i];
+          y[i] = y[i + 1];
+          y[i + 1] = t;
+        }
+        y[i + 1] -= DL[i] * y[i];
+      }
+      y[8] *= rD[8];
+      y[7] = (y[7] - DU[7] * y[8]) * rD[7];
+#pragma unroll
+      for (int i = 6; i >= 0; --i) y[i] = (y[i] - DU[i] * y[i + 1] - DU2[i] * y[i + 2]) * rD[i];
+      for (int w = 0; w < u; ++w) {
+        double lw = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == w) lw = lu[q];
+        if (fabs(lw - lj) > 1e-3 * tn) continue;
+        double dot = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) dot += S(42 + 9 * w + q) * y[q];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) y[q] -= dot * S(42 + 9 * w + q);
+      }
+      double yy = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) yy += y[q] * y[q];
+      if (!(yy > 0.0)) return false;
+      const double iy = rsqrt(yy);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) y[q] *= iy;
+    }
+    // ---- 5. residual |T y - lj y| and orthogonality to the earlier vectors
+    double rr = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      double acc = (d[q] - lj) * y[q];
+      if (q > 0) acc += e[q - 1] * y[q - 1];
+      if (q < 8) acc += e[q] * y[q + 1];
+      rr += acc * acc;
+    }
+    if (!(rr <= 1e-24 * n2)) return false;
+    for (int w = 0; w < u; ++w) {
+      double dot = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) dot += S(42 + 9 * w + q) * y[q];
+      if (!(fabs(dot) <= 1e-12)) return false;
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) S(42 + 9 * u + q) = y[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == u) lu[q] = lj;
+  }
+  // ---- P = M - sum lam x x^T (negative side) or sum max(lam, 0) x x^T,
+  // x = Q y = H_0 ... H_6 y
+#pragma unroll
+  for (int q = 0; q < 45; ++q) P[q] = negside ? ld_reload(msrc + q) : 0.0;
+#pragma unroll 1
+  for (int w = 0; w < nuse; ++w) {
+    double lw = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == w) lw = lu[q];
+    double x[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) x[q] = S(42 + 9 * w + q);
+#pragma unroll
+    for (int k = 6; k >= 0; --k) {
+      double sd = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8 - k; ++q) sd += S(refl_off(k) + q) * x[k + 1 + q];
+      sd *= S(35 + k);
+#pragma unroll
+      for (int q = 0; q < 8 - k; ++q) x[k + 1 + q] -= sd * S(refl_off(k) + q);
+    }
+    const double f = negside ? -lw : fmax(lw, 0.0);
+#pragma unroll
+    for (int a = 0; a < 9; ++a)
+#pragma unroll
+      for (int b = a; b < 9; ++b) P[pk9(a, b)] += f * x[a] * x[b];
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Edge-space (9x9, index 3*edge + coord) Hessian H_D -> vertex blocks.
 //
 // FullProject:    M = (R (x) I) H_D (R^T (x) I), P = Proj9(M), E = W

@@ -540,7 +540,7 @@ class Engine:
     def pcg_path(self) -> str:
         """Kernel path of the last uniform-3x3 solve."""
         ms = np.zeros(16)
-        cnt = np.zeros(3, dtype=np.int64)
+        cnt = np.zeros(4, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
         return {1: "sliced-ELL copy", 2: "row gather"}.get(int(cnt[2]), "general")
 
@@ -551,11 +551,19 @@ class Engine:
 
     def stage_times(self, with_counts: bool = False):
         ms = np.zeros(16)
-        cnt = np.zeros(3, dtype=np.int64)
+        cnt = np.zeros(4, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
         if with_counts:
             return ms, int(cnt[0]), int(cnt[1])
         return ms, int(cnt[0])
+
+    def evd_fallbacks(self) -> int:
+        """Indefinite elements of the last assembly projected by the Jacobi
+        fallback instead of the clamped-eigenpair path."""
+        ms = np.zeros(16)
+        cnt = np.zeros(4, dtype=np.int64)
+        self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
+        return int(cnt[3])
 
 
 class BlockSystem:

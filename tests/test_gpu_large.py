@@ -1,8 +1,10 @@
 """GPU vs the oracle restatement at the BASELINE's large configurations — C4
 (cloth, 301k DoFs, bending at scale) and C5 (the headline pile, 1.02M tets,
-565k DoFs, 181k contact pairs) — on the bench's prepared state (bench.prepare:
-seeded jitter, begin_frame, contact refresh; the oracle refreshes its pairs
-with the reference's all-pairs loop).
+565k DoFs) — on the round-1 jittered rest state (seeded jitter, begin_frame,
+contact refresh: C5 181k pairs, 420 PCG iterations) and on the bench's
+rolled-out state (bench.prepare: 25 frames simulated on the device, then the
+oracle takes the state over, bench.oracle_from).  The oracle refreshes its
+pairs with the reference's all-pairs loop.
 
 Bars: contact pairs, structure checksums and block coordinates
 bit-exact; H values, gradient, diagonal blocks within 1e-9 relative (max|diff| /
@@ -33,20 +35,25 @@ from fixtures import rel  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["c4", "c5"])
+@pytest.fixture(scope="module", params=[("c4", "jitter"), ("c5", "jitter"), ("c5", "rollout")],
+                ids=["c4-jitter", "c5-jitter", "c5-rollout"])
 def pair(request):
-    from bench import prepare
-    g = prepare(request.param, True, "gpu")
-    o = prepare(request.param, True, "oracle")
+    from bench import oracle_from, prepare
+    name, state = request.param
+    g = prepare(name, True, "gpu", state=state)
+    o = prepare(name, True, "oracle", state=state) if state == "jitter" else oracle_from(g, name, True)
     for e in (g.eng, o.eng):
         e.refresh_dynamic()
         e.assemble(True, True)
-    return request.param, g, o
+    yield name, g, o
+    g.eng.close()
+    o.eng.close()
 
 
 def test_large_pairs_structure_values(pair):
     name, g, o = pair
     eg, eo = g.eng, o.eng
+    assert eg.pair_count(g.contact_pairset) > 0
     assert np.array_equal(eg.get_pairs(g.contact_pairset), eo.get_pairs(o.contact_pairset))
     for w in (0, 1):
         hg, ho = eg.hessian(w), eo.hessian(w)

@@ -1,6 +1,6 @@
 """GPU vs the oracle restatement on a large scene (C4 cloth, C5 pile) from the
 bench's prepared state (development aid for tests/test_gpu_large.py; prints
-every comparison).  usage: python tools/parity_large.py c5"""
+every comparison).  usage: python tools/parity_large.py c5 [rollout|jitter]"""
 import os
 import sys
 import time
@@ -11,14 +11,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-from bench import prepare  # noqa: E402
+from bench import oracle_from, prepare  # noqa: E402
 from fixtures import rel  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
+state = sys.argv[2] if len(sys.argv) > 2 else "rollout"
 t0 = time.time()
-g = prepare(name, True, "gpu")
+g = prepare(name, True, "gpu", state=state)
 t1 = time.time()
-o = prepare(name, True, "oracle")
+o = oracle_from(g, name, True) if state == "rollout" else prepare(name, True, "oracle", state=state)
 t2 = time.time()
 print(f"{name}: build+pairs gpu {t1-t0:.1f}s oracle {t2-t1:.1f}s", flush=True)
 eg, eo = g.eng, o.eng
