@@ -194,10 +194,13 @@ struct StencilBatch {
 // ~5k FP64 operations, registers + 552 B of shared memory per thread); an
 // element whose verification fails goes to its energy's fallback list.
 template <int KIND>
-__global__ void __launch_bounds__(kProjStride) k_eval_stencil_b_tri(const __grid_constant__ StencilBatch B,
-                                                                    const int32_t* __restrict__ list,
-                                                                    const double* __restrict__ mbuf) {
+__global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __grid_constant__ StencilBatch B,
+                                                                       const int32_t* __restrict__ list,
+                                                                       const double* __restrict__ mbuf,
+                                                                       double* __restrict__ scratch) {
   extern __shared__ double sm_proj[];
+  const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
+  double* gsc = scratch + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned pre[kStencilBatch + 1];
   pre[0] = 0;
 #pragma unroll
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kProjStride) k_eval_stencil_b_tri(const __grid
     const EnergyDev& E = B.e[j];
     const int64_t slot = B.base[j] + (k - pre[j]);
     double m[45];
-    if (!psd_project9_tri(mbuf + 45 * slot, m, sm_proj + threadIdx.x)) {
+    if (!psd_project9_tri(mbuf + 45 * slot, m, sm_proj + threadIdx.x, gsc, gstride)) {
       const unsigned f = atomicAdd(B.fbcount[j], 1u);
       B.fblist[j][f] = int32_t(k - pre[j]);
       continue;
@@ -1008,11 +1011,16 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
         attr = true;
       }
       const unsigned gt = unsigned(sm_count() * 3);
+      // per-thread reflector scratch; the two static-evaluation streams get
+      // separate halves
+      const size_t per = size_t(kProjScratch) * gt * kProjStride;
+      c.evd_scratch.resize(std::max(c.evd_scratch.n, 2 * per));
+      double* scr = c.evd_scratch.p + (part == 1 ? per : 0);
       if (pending_kind == 0) {
-        k_eval_stencil_b_tri<0><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p);
+        k_eval_stencil_b_tri<0><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr);
         k_eval_stencil_b_fallback<0><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
       } else {
-        k_eval_stencil_b_tri<1><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p);
+        k_eval_stencil_b_tri<1><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr);
         k_eval_stencil_b_fallback<1><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
       }
       YS_LAUNCH_CHECK();

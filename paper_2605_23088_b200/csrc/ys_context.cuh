@@ -263,6 +263,7 @@ struct Context {
   DevBuf<int32_t> evd_list;      // pending element ids
   DevBuf<unsigned int> evd_count;  // per energy: indefinite elements, then Jacobi-fallback elements
   DevBuf<int32_t> evd_fblist;      // fallback elements (local list positions)
+  DevBuf<double> evd_scratch;      // pass-B reflector scratch (per thread, two streams)
   int64_t evd_last = 0;          // indefinite elements of the last assembly (diagnostics)
 
   // profiling

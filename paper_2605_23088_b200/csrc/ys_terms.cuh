@@ -162,7 +162,8 @@ __device__ __forceinline__ int psd_project9(double* a) {
 // ---------------------------------------------------------------------------
 // Clamped-eigenpair projection of a packed 9x9 M (pass B's main path):
 //   1. Householder tridiagonalization T = Q^T M Q, Q = H_0 ... H_6 (the
-//      reflectors go to shared memory: slots [0, 35) v_k, [35, 42) beta_k);
+//      reflectors go to a per-thread global scratch, L2-resident: [0, 35)
+//      v_k, [35, 42) beta_k; d and e of T to shared memory);
 //   2. all eigenvalues of T by implicit QL (Wilkinson-type shift), the sweep
 //      over the unreduced block written as a static loop over i with a
 //      predicate l <= i < m (registers only, small code);
@@ -171,10 +172,10 @@ __device__ __forceinline__ int psd_project9(double* a) {
 //      Sturm count of T at -tau0;
 //   4. eigenvectors only for the clamped side — the k <= 4 negative
 //      eigenvalues (P = M - sum lam x x^T) or else the <= 4 others
-//      (P = sum max(lam, 0) x x^T) — by inverse iteration on T (pivoted
-//      tridiagonal LU, 2 solves; members of a cluster Gram-Schmidt
+//      (P = sum max(lam, 0) x x^T) — by inverse iteration on T (LDL^T of
+//      T - lam I, 2 solves; members of a cluster Gram-Schmidt
 //      orthogonalized against the earlier ones), kept in the T basis in
-//      shared-memory slots [42, 78) and back-transformed with the reflectors
+//      shared-memory slots [0, 36) and back-transformed with the reflectors
 //      when P is formed;
 //   5. verification: every used pair's residual |T y - lam y| <= 1e-12 |M|_F
 //      and used vectors orthogonal to 1e-12.  Then |P - Proj(M)| is bounded
@@ -187,7 +188,8 @@ __device__ __forceinline__ int psd_project9(double* a) {
 // Measured on C5 tets (tools/evd_proto3.py, the same algorithm in numpy):
 // 100 % accepted at the rolled-out and the jittered state, max |P - eigh| /
 // max|M| = 3.7e-15.  ~5k FP64 operations against ~19k for the Jacobi EVD.
-// sm: this thread's slot 0 in a [69][kProjStride] shared array.
+// sm: this thread's slot 0 in a [kProjSlots][kProjStride] shared array; gsc:
+// its slot 0 in a [kProjScratch][gstride] global scratch.
 constexpr int kProjStride = 128;
 
 // Reload of M at the end of the projection: a volatile load, so the compiler
@@ -198,12 +200,16 @@ __device__ __forceinline__ double ld_reload(const double* p) {
   asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-constexpr int kProjSlots = 78;
+constexpr int kProjSlots = 53;  // shared: [0, 36) the used vectors (T basis), [36, 45) d, [45, 53) e
+constexpr int kSlotD = 36, kSlotE = 45;
+constexpr int kProjScratch = 42;  // global, per thread: [0, 35) reflectors v_k, [35, 42) beta_k
 
 __device__ __forceinline__ int refl_off(int k) { return k * 8 - (k * (k - 1)) / 2; }  // sum_{i<k} (8 - i)
 
-__device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc, double* P, double* sm) {
+__device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc, double* P, double* sm,
+                                                 double* gsc, int64_t gstride) {
   auto S = [&](int slot) -> double& { return sm[slot * kProjStride]; };
+  auto G = [&](int slot) -> double& { return gsc[slot * gstride]; };
   double a[45];
   double n2 = 0.0;
 #pragma unroll
@@ -253,13 +259,17 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
       for (int j = 0; j <= i; ++j) a[pk9(k + 1 + i, k + 1 + j)] -= v[i] * p[j] + p[i] * v[j];
     e[k] = nx != 0.0 ? alpha : 0.0;
 #pragma unroll
-    for (int i = 0; i < m; ++i) S(refl_off(k) + i) = v[i];
-    S(35 + k) = beta;
+    for (int i = 0; i < m; ++i) G(refl_off(k) + i) = v[i];
+    G(35 + k) = beta;
   }
   e[7] = a[pk9(8, 7)];
   double d[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) d[i] = a[pk9(i, i)];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) S(kSlotD + i) = d[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) S(kSlotE + i) = e[i];
   // ---- 2. eigenvalues (implicit QL on copies).  One loop iteration = one QL
   // sweep of this lane's current unreduced block [l, m]; lanes deflate
   // independently (the warp runs max over its lanes of the total sweep count,
@@ -355,19 +365,32 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
   int kneg = 0;
 #pragma unroll
   for (int i = 0; i < 9; ++i) kneg += lam[i] < -tau0;
+  // the used eigenvalues (the clamped side), lam dies here
+  const bool negside = kneg <= 4;
+  const int nuse = negside ? kneg : 9 - kneg;
+  double lu[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int sel = negside ? u : kneg + u;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+      if (i == sel) lu[u] = lam[i];
+  }
   // ---- 3. Sturm count of T at -tau0 must agree
   double tn = 0.0;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) tn = fmax(tn, fabs(d[i]) + (i < 8 ? fabs(e[i]) : 0.0) + (i > 0 ? fabs(e[i - 1]) : 0.0));
+  for (int i = 0; i < 9; ++i)
+    tn = fmax(tn, fabs(S(kSlotD + i)) + (i < 8 ? fabs(S(kSlotE + i)) : 0.0) + (i > 0 ? fabs(S(kSlotE + i - 1)) : 0.0));
   const double pivmin = 1e-300 + 2.2e-19 * tn;
   {
     int cnt = 0;
-    double q = d[0] + tau0;
+    double q = S(kSlotD) + tau0;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
 #pragma unroll
     for (int i = 1; i < 9; ++i) {
-      q = d[i] + tau0 - e[i - 1] * e[i - 1] / q;
+      const double ei = S(kSlotE + i - 1);
+      q = S(kSlotD + i) + tau0 - ei * ei / q;
       if (fabs(q) < pivmin) q = -pivmin;
       cnt += q < 0.0;
     }
@@ -378,75 +401,42 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
     for (int q = 0; q < 45; ++q) P[q] = ld_reload(msrc + q);
     return true;
   }
-  // clamped side: the kneg <= 4 negative eigenvalues, else the <= 4 others
-  const bool negside = kneg <= 4;
-  const int nuse = negside ? kneg : 9 - kneg;
   // ---- 4. eigenvectors of T for the used eigenvalues (T basis, smem slots
   // [42, 78)); members of a cluster (|lam_u - lam_w| <= 1e-3 |T|) are
   // Gram-Schmidt orthogonalized against the earlier ones after every solve
-  double lu[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 1
   for (int u = 0; u < nuse; ++u) {
-    const int sel = negside ? u : kneg + u;
     double lj = 0.0;
 #pragma unroll
-    for (int i = 0; i < 9; ++i)
-      if (i == sel) lj = lam[i];
-    // pivoted LU of T - lj I (LAPACK dgttrf layout)
-    double D[9], DL[8], DU[8], DU2[7], rD[9];
-    bool piv[8];
+    for (int q = 0; q < 4; ++q)
+      if (q == u) lj = lu[q];
+    // LDL^T of T - lj I without pivoting (tiny pivots replaced by pivmin;
+    // the verification below catches any loss of accuracy)
+    double rq[9], ll[8];
+    {
+      double q = S(kSlotD) - lj;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) D[i] = d[i] - lj;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      DL[i] = e[i];
-      DU[i] = e[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 7; ++i) DU2[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      piv[i] = !(fabs(D[i]) >= fabs(DL[i]));
-      if (!piv[i]) {
-        if (D[i] == 0.0) D[i] = pivmin;
-        rD[i] = 1.0 / D[i];
-        const double fact = DL[i] * rD[i];
-        DL[i] = fact;
-        D[i + 1] -= fact * DU[i];
-      } else {
-        rD[i] = 1.0 / DL[i];
-        const double fact = D[i] * rD[i];
-        D[i] = DL[i];
-        DL[i] = fact;
-        const double temp = DU[i];
-        DU[i] = D[i + 1];
-        D[i + 1] = temp - fact * D[i + 1];
-        if (i < 7) {
-          DU2[i] = DU[i + 1];
-          DU[i + 1] = -fact * DU[i + 1];
-        }
+      for (int i = 0; i < 8; ++i) {
+        if (fabs(q) < pivmin) q = pivmin;
+        rq[i] = 1.0 / q;
+        const double ei = S(kSlotE + i);
+        ll[i] = ei * rq[i];
+        q = S(kSlotD + i + 1) - lj - ll[i] * ei;
       }
+      if (fabs(q) < pivmin) q = pivmin;
+      rq[8] = 1.0 / q;
     }
-    if (D[8] == 0.0) D[8] = pivmin;
-    rD[8] = 1.0 / D[8];
     double y[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) y[i] = 1.0 / 3.0 + ((i + 2 * u) % 9 == 0 ? 0.25 : 0.0);
 #pragma unroll
     for (int itr = 0; itr < 2; ++itr) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (piv[i]) {
-          const double t = y[i];
-          y[i] = y[i + 1];
-          y[i + 1] = t;
-        }
-        y[i + 1] -= DL[i] * y[i];
-      }
-      y[8] *= rD[8];
-      y[7] = (y[7] - DU[7] * y[8]) * rD[7];
+      for (int i = 1; i < 9; ++i) y[i] -= ll[i - 1] * y[i - 1];
 #pragma unroll
-      for (int i = 6; i >= 0; --i) y[i] = (y[i] - DU[i] * y[i + 1] - DU2[i] * y[i + 2]) * rD[i];
+      for (int i = 0; i < 9; ++i) y[i] *= rq[i];
+#pragma unroll
+      for (int i = 7; i >= 0; --i) y[i] -= ll[i] * y[i + 1];
       for (int w = 0; w < u; ++w) {
         double lw = 0.0;
 #pragma unroll
@@ -455,9 +445,9 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
         if (fabs(lw - lj) > 1e-3 * tn) continue;
         double dot = 0.0;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) dot += S(42 + 9 * w + q) * y[q];
+        for (int q = 0; q < 9; ++q) dot += S(9 * w + q) * y[q];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) y[q] -= dot * S(42 + 9 * w + q);
+        for (int q = 0; q < 9; ++q) y[q] -= dot * S(9 * w + q);
       }
       double yy = 0.0;
 #pragma unroll
@@ -471,51 +461,58 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
     double rr = 0.0;
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
-      double acc = (d[q] - lj) * y[q];
-      if (q > 0) acc += e[q - 1] * y[q - 1];
-      if (q < 8) acc += e[q] * y[q + 1];
+      double acc = (S(kSlotD + q) - lj) * y[q];
+      if (q > 0) acc += S(kSlotE + q - 1) * y[q - 1];
+      if (q < 8) acc += S(kSlotE + q) * y[q + 1];
       rr += acc * acc;
     }
     if (!(rr <= 1e-24 * n2)) return false;
     for (int w = 0; w < u; ++w) {
       double dot = 0.0;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) dot += S(42 + 9 * w + q) * y[q];
+      for (int q = 0; q < 9; ++q) dot += S(9 * w + q) * y[q];
       if (!(fabs(dot) <= 1e-12)) return false;
     }
 #pragma unroll
-    for (int q = 0; q < 9; ++q) S(42 + 9 * u + q) = y[q];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q == u) lu[q] = lj;
+    for (int q = 0; q < 9; ++q) S(9 * u + q) = y[q];
   }
-  // ---- P = M - sum lam x x^T (negative side) or sum max(lam, 0) x x^T,
-  // x = Q y = H_0 ... H_6 y
-#pragma unroll
-  for (int q = 0; q < 45; ++q) P[q] = negside ? ld_reload(msrc + q) : 0.0;
+  // ---- back-transform the used vectors in place: x = Q y = H_0 ... H_6 y
 #pragma unroll 1
   for (int w = 0; w < nuse; ++w) {
-    double lw = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q == w) lw = lu[q];
     double x[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) x[q] = S(42 + 9 * w + q);
+    for (int q = 0; q < 9; ++q) x[q] = S(9 * w + q);
 #pragma unroll
     for (int k = 6; k >= 0; --k) {
       double sd = 0.0;
 #pragma unroll
-      for (int q = 0; q < 8 - k; ++q) sd += S(refl_off(k) + q) * x[k + 1 + q];
-      sd *= S(35 + k);
+      for (int q = 0; q < 8 - k; ++q) sd += G(refl_off(k) + q) * x[k + 1 + q];
+      sd *= G(35 + k);
 #pragma unroll
-      for (int q = 0; q < 8 - k; ++q) x[k + 1 + q] -= sd * S(refl_off(k) + q);
+      for (int q = 0; q < 8 - k; ++q) x[k + 1 + q] -= sd * G(refl_off(k) + q);
     }
-    const double f = negside ? -lw : fmax(lw, 0.0);
 #pragma unroll
-    for (int a = 0; a < 9; ++a)
+    for (int q = 0; q < 9; ++q) S(9 * w + q) = x[q];
+  }
+  // ---- P = M - sum lam x x^T (negative side) or sum max(lam, 0) x x^T,
+  // row by row with the vectors read from shared memory (P is the only
+  // 45-register array live here)
+  double fw[4];
 #pragma unroll
-      for (int b = a; b < 9; ++b) P[pk9(a, b)] += f * x[a] * x[b];
+  for (int w = 0; w < 4; ++w) fw[w] = w < nuse ? (negside ? -lu[w] : fmax(lu[w], 0.0)) : 0.0;
+#pragma unroll
+  for (int a = 0; a < 9; ++a) {
+    double xa[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) xa[w] = w < nuse ? fw[w] * S(9 * w + a) : 0.0;
+#pragma unroll
+    for (int b = a; b < 9; ++b) {
+      double acc = negside ? ld_reload(msrc + pk9(a, b)) : 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (w < nuse) acc += xa[w] * S(9 * w + b);
+      P[pk9(a, b)] = acc;
+    }
   }
   return true;
 }

@@ -104,7 +104,11 @@ def sturm(d, e, x, pivmin):
     return cnt
 
 
-def inv_iter(d, e, sig, pivmin, its=3):
+ITS = int(os.environ.get('EVD_ITS', '2'))
+
+
+def inv_iter(d, e, sig, pivmin, its=None):
+    its = ITS if its is None else its
     D = d - sig
     DL = e.copy()
     DU = e.copy()
@@ -143,6 +147,35 @@ def inv_iter(d, e, sig, pivmin, its=3):
             b[i] = (b[i] - DU[i] * b[i + 1] - DU2[i] * b[i + 2]) / D[i]
         y = b / math.sqrt(b @ b)
     return y
+
+
+def inv_iter_ldl(d, e, sig, pivmin, its=None):
+    """Non-pivoted LDL^T of T - sig I (tiny pivots replaced by pivmin)."""
+    its = ITS if its is None else its
+    q = np.zeros(9)
+    l = np.zeros(8)
+    q[0] = d[0] - sig
+    for i in range(1, 9):
+        if abs(q[i - 1]) < pivmin:
+            q[i - 1] = pivmin
+        l[i - 1] = e[i - 1] / q[i - 1]
+        q[i] = d[i] - sig - l[i - 1] * e[i - 1]
+    if abs(q[8]) < pivmin:
+        q[8] = pivmin
+    y = np.full(9, 1.0 / 3.0)
+    for _ in range(its):
+        z = y.copy()
+        for i in range(1, 9):
+            z[i] -= l[i - 1] * z[i - 1]
+        z /= q
+        for i in range(7, -1, -1):
+            z[i] -= l[i] * z[i + 1]
+        y = z / math.sqrt(z @ z)
+    return y
+
+
+if os.environ.get("EVD_LDL"):
+    inv_iter = inv_iter_ldl  # noqa: F811
 
 
 def back(V, beta, y):
