@@ -160,16 +160,21 @@ __global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const doubl
   }
   const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
   if (full) edge_to_projection_space(hd);
-  if (cholesky_pd9(hd)) {
-    expand_vertex_blocks(hd, full, wr);  // M is PD: the projection is M itself
+  // M goes to the element's slot first; the positive-definiteness test then
+  // factors the registers in place (no second 45-register copy)
+  double* m = mbuf + 45 * i;
+#pragma unroll
+  for (int q = 0; q < 45; ++q) m[q] = hd[q];
+  if (cholesky_pd9_inplace(hd)) {
+    // M is PD: the projection is M itself (reloaded from its slot)
+#pragma unroll
+    for (int q = 0; q < 45; ++q) hd[q] = ld_reload(m + q);
+    expand_vertex_blocks(hd, full, wr);
     return;
   }
   // indefinite: pass B projects M and writes the vertex blocks
   const unsigned k = atomicAdd(count, 1u);
   list[k] = int32_t(i);
-  double* m = mbuf + 45 * int64_t(k);
-#pragma unroll
-  for (int q = 0; q < 45; ++q) m[q] = hd[q];
 }
 
 // Pass B: Jacobi EVD + clamp + reconstruction for the compacted indefinite
@@ -208,17 +213,22 @@ __global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __g
   const unsigned total = pre[kStencilBatch];
   for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += gridDim.x * blockDim.x) {
     int j = 0;
+    unsigned prej = 0;  // pre[j] by a static select (no local-memory array)
 #pragma unroll
-    for (int q = 1; q < kStencilBatch; ++q) j += k >= pre[q] ? 1 : 0;
+    for (int q = 1; q < kStencilBatch; ++q)
+      if (k >= pre[q]) {
+        j = q;
+        prej = pre[q];
+      }
     const EnergyDev& E = B.e[j];
-    const int64_t slot = B.base[j] + (k - pre[j]);
+    const int64_t slot = B.base[j] + (k - prej);
+    const int64_t i = list[slot];
     double m[45];
-    if (!psd_project9_tri(mbuf + 45 * slot, m, sm_proj + threadIdx.x, gsc, gstride)) {
+    if (!psd_project9_tri(mbuf + 45 * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
       const unsigned f = atomicAdd(B.fbcount[j], 1u);
-      B.fblist[j][f] = int32_t(k - pre[j]);
+      B.fblist[j][f] = int32_t(k - prej);
       continue;
     }
-    const int64_t i = list[slot];
     const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
     const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
     const bool full = KIND == 1 || E.mode != YS_PROJECT_REDUCED;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_fallback(const __grid_co
     const int64_t slot = B.base[j] + B.fblist[j][k - pre[j]];
     const int64_t i = list[slot];
     double m[45];
-    const double* src = mbuf + 45 * slot;
+    const double* src = mbuf + 45 * (B.base[j] + i);
 #pragma unroll
     for (int q = 0; q < 45; ++q) m[q] = src[q];
     psd_project9(m);
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_batch(const __grid_const
     const int64_t slot = B.base[j] + (k - pre[j]);
     const int64_t i = list[slot];
     double m[45];
-    const double* src = mbuf + 45 * slot;
+    const double* src = mbuf + 45 * (B.base[j] + i);
 #pragma unroll
     for (int q = 0; q < 45; ++q) m[q] = src[q];
     psd_project9(m);

@@ -302,35 +302,36 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
       if (!__any_sync(__activemask(), active)) break;
       if (sweep == 120) return false;
       if (active) {
+        // d_l, e_l, d_{l+1}, d_m by arithmetic blends (a select chain gets
+        // turned back into an indexed load, which moves lam to local memory)
         double dl = 0.0, dl1 = 0.0, el = 0.0, dm = 0.0;
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
-          if (i == l) {
-            dl = lam[i];
-            el = ee[i];
-          }
-          if (i == l + 1) dl1 = lam[i];
-          if (i == m) dm = lam[i];
+          const double w0 = i == l ? 1.0 : 0.0, w1 = i == l + 1 ? 1.0 : 0.0, wm = i == m ? 1.0 : 0.0;
+          dl = fma(w0, lam[i], dl);
+          el = fma(w0, ee[i], el);
+          dl1 = fma(w1, lam[i], dl1);
+          dm = fma(wm, lam[i], dm);
         }
-        double g = (dl1 - dl) / (2.0 * el);
-        double r = hypot(g, 1.0);
-        g = dm - dl + el / (g + copysign(r, g));
+        // Wilkinson-type shift: with h = d_{l+1} - d_l,
+        //   e_l / (g + sgn(g) sqrt(g^2 + 1)), g = h / (2 e_l)
+        //   = 2 e_l^2 / (h + sgn(h) sqrt(h^2 + 4 e_l^2))   (one sqrt, one division)
+        const double h = dl1 - dl;
+        const double rh = sqrt(h * h + 4.0 * el * el);
+        double g = dm - dl + 2.0 * el * el / (h + copysign(rh, h));
+        double r;
         double s = 1.0, c = 1.0, pp = 0.0;
 #pragma unroll
         for (int i = 7; i >= 0; --i) {
           if (i < m && i >= l) {
             const double f = s * ee[i], b = c * ee[i];
-            const double r2 = f * f + g * g;
-            if (r2 == 0.0) {
-              ee[i + 1] = 0.0;
-              s = 0.0;
-              c = 1.0;
-            } else {
-              const double ir = rsqrt(r2);
-              ee[i + 1] = r2 * ir;
-              s = f * ir;
-              c = g * ir;
-            }
+            // r2 == 0 (f = g = 0) only in degenerate arithmetic; the floor
+            // keeps it finite and the verification catches any damage
+            const double r2 = fmax(f * f + g * g, 1e-300);
+            const double ir = rsqrt(r2);
+            ee[i + 1] = r2 * ir;
+            s = f * ir;
+            c = g * ir;
             g = lam[i + 1] - pp;
             r = (lam[i] - g) * s + 2.0 * c * b;
             pp = s * r;
@@ -528,33 +529,41 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
 
 // In place: hd <- (R (x) I) hd (R^T (x) I)   (blocks, HD_{ii'} = HD_{i'i}^T)
 __device__ __forceinline__ void edge_to_projection_space(double* hd) {
+  // one flat loop over the packed entries (the nested block form was left
+  // partly rolled by the compiler, which put hd in local memory)
   double m[45];
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
+  for (int p = 0; p < 45; ++p) {
+    int r = 0, c = 0;  // packed (row, col) of p, row <= col
 #pragma unroll
-    for (int b = a; b < 3; ++b)
+    for (int rr = 0; rr < 9; ++rr)
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          if (a == b && kk < k) continue;
-          double acc = 0.0;
-#pragma unroll
-          for (int i = a; i < 3; ++i)
-#pragma unroll
-            for (int ip = b; ip < 3; ++ip) acc += kR(a, i) * kR(b, ip) * hd[pk9(3 * i + k, 3 * ip + kk)];
-          m[pk9(3 * a + k, 3 * b + kk)] = acc;
+      for (int cc = rr; cc < 9; ++cc)
+        if (pk9(rr, cc) == p) {
+          r = rr;
+          c = cc;
         }
+    const int a = r / 3, k = r % 3, b = c / 3, kk = c % 3;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int ip = 0; ip < 3; ++ip)
+        if (i >= a && ip >= b) acc += kR(a, i) * kR(b, ip) * hd[pk9(3 * i + k, 3 * ip + kk)];
+    m[p] = acc;
+  }
 #pragma unroll
   for (int i = 0; i < 45; ++i) hd[i] = m[i];
 }
 
-template <class Writer>
-__device__ __forceinline__ void expand_vertex_blocks(const double* hd, bool full, const Writer& wr) {
+template <bool FULL, class Writer>
+__device__ __forceinline__ void expand_vb(const double* hd, const Writer& wr) {
 #pragma unroll
-  for (int a = 0, pair = 0; a < 4; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = a; b < 4; ++b, ++pair)
+    for (int b = 0; b < 4; ++b) {
+      if (b < a) continue;
+      const int pair = a * 4 - (a * (a - 1)) / 2 + (b - a);
 #pragma unroll
       for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -565,14 +574,24 @@ __device__ __forceinline__ void expand_vertex_blocks(const double* hd, bool full
           for (int i = 0; i < 3; ++i)
 #pragma unroll
             for (int ip = 0; ip < 3; ++ip) {
-              const double ea = full ? kW(a, i) : kST(a, i);
-              const double eb = full ? kW(b, ip) : kST(b, ip);
+              const double ea = FULL ? kW(a, i) : kST(a, i);
+              const double eb = FULL ? kW(b, ip) : kST(b, ip);
               if (ea == 0.0 || eb == 0.0) continue;
               acc += ea * eb * hd[pk9(3 * i + k, 3 * ip + kk)];
             }
           wr(pair, k, kk, acc);
           if (a == b && kk != k) wr(pair, kk, k, acc);
         }
+    }
+}
+
+// the projection-space map is a compile-time choice inside (zero terms fold)
+template <class Writer>
+__device__ __forceinline__ void expand_vertex_blocks(const double* hd, bool full, const Writer& wr) {
+  if (full)
+    expand_vb<true>(hd, wr);
+  else
+    expand_vb<false>(hd, wr);
 }
 
 // Positive-definiteness test by Cholesky on a copy: true iff every pivot is
@@ -596,6 +615,33 @@ __device__ __forceinline__ bool cholesky_pd9(const double* m) {
       double v = l[pk9(i, j)];
 #pragma unroll
       for (int k = 0; k < j; ++k) v -= l[pk9(i, k)] * l[pk9(j, k)];
+      l[pk9(i, j)] = v * inv;
+    }
+  }
+  return pd;
+}
+
+// In place (m is destroyed): true iff every Cholesky pivot is positive.
+__device__ __forceinline__ bool cholesky_pd9_inplace(double* l) {
+  // constant loop bounds with guards: fully unrolled, l stays in registers
+  bool pd = true;
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    double d = l[pk9(j, j)];
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (k < j) d -= l[pk9(j, k)] * l[pk9(j, k)];
+    pd = pd && (d > 0.0);
+    const double ljj = sqrt(d > 0.0 ? d : 1.0);
+    l[pk9(j, j)] = ljj;
+    const double inv = 1.0 / ljj;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (i <= j) continue;
+      double v = l[pk9(i, j)];
+#pragma unroll
+      for (int k = 0; k < 9; ++k)
+        if (k < j) v -= l[pk9(i, k)] * l[pk9(j, k)];
       l[pk9(i, j)] = v * inv;
     }
   }
@@ -700,7 +746,8 @@ __device__ __forceinline__ void snh_local(const double x[12], const double binv[
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int ip = i; ip < 3; ++ip) {
+    for (int ip = 0; ip < 3; ++ip) {
+      if (ip < i) continue;
       double a[9];  // A_{ii'}[j][j']
 #pragma unroll
       for (int j = 0; j < 3; ++j)
