@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __g
     double m[45];
     if (!psd_project9_tri(mbuf + 45 * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
       const unsigned f = atomicAdd(B.fbcount[j], 1u);
-      B.fblist[j][f] = int32_t(k - prej);
+      B.fblist[j][f] = int32_t(i);
       continue;
     }
     const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
@@ -253,8 +253,7 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_fallback(const __grid_co
 #pragma unroll
     for (int q = 1; q < kStencilBatch; ++q) j += k >= pre[q] ? 1 : 0;
     const EnergyDev& E = B.e[j];
-    const int64_t slot = B.base[j] + B.fblist[j][k - pre[j]];
-    const int64_t i = list[slot];
+    const int64_t i = B.fblist[j][k - pre[j]];  // element id
     double m[45];
     const double* src = mbuf + 45 * (B.base[j] + i);
 #pragma unroll
