@@ -202,7 +202,8 @@ template <int KIND>
 __global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __grid_constant__ StencilBatch B,
                                                                        const int32_t* __restrict__ list,
                                                                        const double* __restrict__ mbuf,
-                                                                       double* __restrict__ scratch) {
+                                                                       double* __restrict__ scratch,
+                                                                       int force_fallback) {
   extern __shared__ double sm_proj[];
   const int64_t gstride = int64_t(gridDim.x) * blockDim.x;
   double* gsc = scratch + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __g
     const int64_t slot = B.base[j] + (k - prej);
     const int64_t i = list[slot];
     double m[45];
-    if (!psd_project9_tri(mbuf + 45 * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
+    if (force_fallback || !psd_project9_tri(mbuf + 45 * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
       const unsigned f = atomicAdd(B.fbcount[j], 1u);
       B.fblist[j][f] = int32_t(i);
       continue;
@@ -1026,10 +1027,10 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
       c.evd_scratch.resize(std::max(c.evd_scratch.n, 2 * per));
       double* scr = c.evd_scratch.p + (part == 1 ? per : 0);
       if (pending_kind == 0) {
-        k_eval_stencil_b_tri<0><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr);
+        k_eval_stencil_b_tri<0><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr, c.evd_mode == 2);
         k_eval_stencil_b_fallback<0><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
       } else {
-        k_eval_stencil_b_tri<1><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr);
+        k_eval_stencil_b_tri<1><<<gt, kProjStride, smem, s>>>(B, c.evd_list.p, c.evd_m.p, scr, c.evd_mode == 2);
         k_eval_stencil_b_fallback<1><<<sm_count(), 128, 0, s>>>(B, c.evd_list.p, c.evd_m.p);
       }
       YS_LAUNCH_CHECK();

@@ -1293,7 +1293,8 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
     const std::string n = name ? name : "";
     if (n == "overlap") c->overlap = value != 0;
     else if (n == "eval_evd") {
-      if (value != 0 && value != 1) fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi) or 1 (clamped eigenpairs)");
+      if (value < 0 || value > 2)
+        fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi), 1 (clamped eigenpairs) or 2 (every element through the fallback)");
       c->evd_mode = int(value);
     } else fail(YS_ERR_VALIDATION, "unknown option '" + n + "'");
   });

@@ -269,7 +269,8 @@ struct Context {
   // profiling
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
-  int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only
+  int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only,
+                       // 2 every element handed to the fallback list (tests)
   double stage_ms[8] = {0};
   double pcg_phase_ms[8] = {0};
   int64_t launches = 0;
