@@ -12,8 +12,8 @@ Newton iteration because each pair refresh bumps the dynamic epoch).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
 
 N > 1 (torchrun): the same scene on every rank, solved by the row-partitioned
-multi-GPU PCG over NCCL ("strong": evaluation and assembly replicated, the PCG
-rows split across ranks).
+multi-GPU PCG over NCCL ("strong": each rank evaluates the static stencil
+instances touching its rows and solves its rows).
 """
 from __future__ import annotations
 
@@ -444,7 +444,7 @@ def main():
                    "prepared_frames": getattr(sim, "prepared_frames", 0),
                    "prepare_s": round(t_prep, 2),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
-                   "parallelism": f"pcg-rows{world} (eval/assembly replicated)" if world > 1 else "single"},
+                   "parallelism": f"rows{world}: owned-row evaluation + row-partitioned PCG" if world > 1 else "single"},
         "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else
                      "row-partitioned PCG (k_dspmv_sell / k_dupdate per rank + NCCL allgather)",
                      "bound": "hbm", "achieved": pcg_gbs, "peak": peak, "unit": "GB/s", "frac": pcg_gbs / peak,

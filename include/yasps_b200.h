@@ -278,6 +278,10 @@ int ys_dist_finalize(ys_context* ctx);
  * boundaries), this rank's halo rows received per iteration, export rows sent. */
 int ys_dist_info(ys_context* ctx, int32_t* rank, int32_t* nranks, int64_t* bounds, int64_t* halo_rows,
                  int64_t* export_rows);
+/* Owned-row evaluation of the distributed solve: the static stencil (SNH,
+ * bending) instances this rank evaluates (those touching its rows; the
+ * partition comes from the static structure) and the scene's total. */
+int ys_dist_eval_counts(ys_context* ctx, int64_t* evaluated, int64_t* total);
 
 /* ------------------------------------------------------------------------
  * Benchmark hooks: per-stage device times of the last minimize_step, measured

@@ -1580,9 +1580,10 @@ static void dist_pcg(yo_context* c, double tol, int64_t max_iter, double* x, int
   const int64_t NB = c->nblk, s = c->s;
   for (int64_t b = 0; b < NB; ++b)
     if (c->brc[b] != 3) fail(c, YS_ERR_VALIDATION, "distributed PCG supports uniform 3x3 block systems only");
-  /* partition */
+  /* partition: the static structure's entries (fixed across Newton
+   * iterations, so the device knows each rank's instances before evaluating) */
   int64_t* W = xcalloc((size_t)NB + 1, sizeof(int64_t));
-  for (int w = 0; w < 2; ++w)
+  for (int w = 0; w < 1; ++w)
     for (int64_t bi = 0; bi < c->H[w].nb; ++bi) {
       W[c->H[w].row[bi] / 3 + 1] += 1;
       if (c->H[w].row[bi] != c->H[w].col[bi]) W[c->H[w].col[bi] / 3 + 1] += 1;
@@ -2722,6 +2723,18 @@ int yo_dist_init_host(yo_context* c, int32_t rank, int32_t nranks, ys_allgather_
 int yo_dist_finalize(yo_context* c) {
   API_BEGIN(c);
   c->dist_on = 0;
+  API_END;
+}
+
+/* The oracle evaluates every instance on every rank (the device evaluates
+ * only the instances touching its rows; the solve is the same). */
+int yo_dist_eval_counts(yo_context* c, int64_t* evaluated, int64_t* total) {
+  API_BEGIN(c);
+  int64_t all = 0;
+  for (int ei = 0; ei < c->ne; ++ei)
+    if (!c->e[ei].dynamic && (c->e[ei].kind == K_SNH || c->e[ei].kind == K_BENDING)) all += c->e[ei].n;
+  if (evaluated) *evaluated = all;
+  if (total) *total = all;
   API_END;
 }
 

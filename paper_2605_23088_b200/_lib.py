@@ -147,12 +147,13 @@ _SIGS = {
     "dist_init_host": [_P, _I32, _I32, ALLGATHER_FN, _P],
     "dist_finalize": [_P],
     "dist_info": [_P, _PI32, _PI32, _PI64, _PI64, _PI64],
+    "dist_eval_counts": [_P, _PI64, _PI64],
 }
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
 OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream", "set_option", "dist_unique_id",
-            "dist_init_nccl"}
+            "dist_init_nccl", "dist_eval_counts"}
 
 
 class Library:

@@ -131,9 +131,12 @@ __global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const doubl
                                                         int want_h, double* __restrict__ hc,
                                                         double* __restrict__ gc, int* err,
                                                         unsigned int* __restrict__ count,
-                                                        int32_t* __restrict__ list, double* __restrict__ mbuf) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= E.n) return;
+                                                        int32_t* __restrict__ list, double* __restrict__ mbuf,
+                                                        const int32_t* __restrict__ sel, int64_t nsel) {
+  // sel: the instances to evaluate (the distributed solve's owned-row subset), else all
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= (sel ? nsel : E.n)) return;
+  const int64_t i = sel ? int64_t(sel[t]) : t;
   double x[12];
   int32_t gs[4];
   load_stencil(E, X, i, x, gs);
@@ -1056,12 +1059,19 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
         int32_t* lst = c.evd_list.p + evd_base[id];
         double* mb = c.evd_m.p + 45 * evd_base[id];
         const int kind = e.kind == K_SNH ? 0 : 1;
+        // distributed solve: only the instances touching this rank's rows
+        const bool part_sel = c.dist.kind && c.dist.nranks > 1 && c.dist.have_static &&
+                              id < c.dist.nsel_e.size() && c.dist.nsel_e[id] >= 0;
+        const int32_t* sel = part_sel ? c.dist.sel[id].p : nullptr;
+        const int64_t nsel = part_sel ? c.dist.nsel_e[id] : e.n;
+        const unsigned gsel = grid_for(nsel, 128);
         if (kind == 0)
-          k_eval_stencil_a<0><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
-                                                 lst, mb);
+          k_eval_stencil_a<0><<<gsel, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
+                                                   lst, mb, sel, nsel);
         else
-          k_eval_stencil_a<1><<<ga, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
-                                                 lst, mb);
+          k_eval_stencil_a<1><<<gsel, 128, 0, s>>>(E, c.X.p, proj, wh, st.hcontrib.p, st.gcontrib.p, c.errflag.p, cnt,
+                                                   lst, mb, sel, nsel);
+        (void)ga;
         YS_LAUNCH_CHECK();
         if (pass_b) {
           if (pending_kind != kind || int(pending.size()) == kStencilBatch) flush();
@@ -1272,8 +1282,14 @@ void ctx_build_preconditioner(Context& c) {
   cudaStream_t s = c.stream;
   c.flagsum.resize(4);
   k_flag_init<<<1, 1, 0, s>>>(c.flagsum.p + 1);
-  k_flag_summary<<<int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.NB, kTB), 4 * sm_count()))), kTB, 0, s>>>(
-      c.bflag.p, c.NB, c.flagsum.p + 1);
+  // distributed solve: only this rank's rows are assembled (and solved)
+  int64_t f0 = 0, f1 = c.NB;
+  if (c.dist.kind && c.dist.nranks > 1 && c.dist.have_static) {
+    f0 = c.dist.sbounds[size_t(c.dist.rank)];
+    f1 = c.dist.sbounds[size_t(c.dist.rank) + 1];
+  }
+  k_flag_summary<<<int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(f1 - f0, kTB), 4 * sm_count()))), kTB, 0, s>>>(
+      c.bflag.p + f0, f1 - f0, c.flagsum.p + 1);
   YS_LAUNCH_CHECK();
   YS_CUDA(cudaMemcpyAsync(c.flagsum.p, c.errflag.p, sizeof(int), cudaMemcpyDeviceToDevice, s));
   int* h = reinterpret_cast<int*>(pinned_buf(c));
@@ -1285,7 +1301,7 @@ void ctx_build_preconditioner(Context& c) {
     fail(YS_ERR_NUMERICAL, "division by zero");
   }
   if (h[2] != INT_MAX) {
-    const int64_t b = h[2];
+    const int64_t b = f0 + h[2];
     int32_t st = 0, rc = 0;
     YS_CUDA(cudaMemcpyAsync(&st, c.bstart.p + b, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     YS_CUDA(cudaMemcpyAsync(&rc, c.brc.p + b, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

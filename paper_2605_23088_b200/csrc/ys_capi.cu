@@ -871,6 +871,7 @@ int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys
     // stream while the dynamic group is rebuilt (whose host synchronisations
     // would otherwise leave the device idle); ys_set_option("overlap", 0):
     // sequential (bitwise the same step, tested).
+    if (c->dist.kind && c->dist.nranks > 1) ctx_dist_static_plan(*c);  // owned-row instance lists (once)
     const bool overlap = c->overlap;
     bool dyn_stencil = false;
     for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
@@ -1285,6 +1286,18 @@ int ys_dist_info(ys_context* c, int32_t* rank, int32_t* nranks, int64_t* bounds,
     const int64_t mine = have ? d.exp_off[d.rank + 1] - d.exp_off[d.rank] : 0;
     if (halo_rows) *halo_rows = have ? d.exp_off[d.nranks] - mine : 0;
     if (export_rows) *export_rows = mine;
+  });
+}
+
+int ys_dist_eval_counts(ys_context* c, int64_t* evaluated, int64_t* total) {
+  return guarded(c, [&] {
+    const DistState& d = c->dist;
+    const bool part = d.kind && d.nranks > 1 && d.have_static;
+    int64_t all = 0;
+    for (auto& e : c->energies)
+      if (!e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING)) all += e.n;
+    if (evaluated) *evaluated = part ? d.eval_owned : all;
+    if (total) *total = all;
   });
 }
 

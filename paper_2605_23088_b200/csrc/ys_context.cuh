@@ -178,6 +178,15 @@ struct DistState {
   DevBuf<int32_t> nsel;
   DevBuf<double> send, recv, dsend, dall;
   std::vector<double> hsend, hrecv;   // host transport staging
+  // Owned-row evaluation: the partition comes from the static structure (so
+  // it is known before the step's evaluation and fixed across iterations);
+  // each static stencil energy evaluates only the instances touching this
+  // rank's rows (boundary instances on both sides).
+  bool have_static = false;
+  std::vector<int64_t> sbounds;               // nranks + 1 block-row boundaries
+  std::vector<DevBuf<int32_t>> sel;           // per energy: selected instances (empty: all)
+  std::vector<int64_t> nsel_e;                // per energy: count (-1: all)
+  int64_t eval_owned = 0, eval_total = 0;     // static stencil instances evaluated / in the scene
 };
 
 struct Context {
@@ -311,6 +320,7 @@ void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats
 void ctx_dist_unique_id(unsigned char* id);
 void ctx_dist_init_nccl(Context& c, int rank, int nranks, const unsigned char* id);
 void ctx_dist_finalize(Context& c);
+void ctx_dist_static_plan(Context& c);  // partition + owned-row instance lists (once)
 uint64_t structure_checksum(Context& c, Structure& st, int64_t total_dofs);
 void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed,
                        int64_t* n_pairs);

@@ -406,9 +406,10 @@ void build_plan(Context& c) {
   const bool has1 = c.S[1].n_blocks > 0;
   d.dbounds.resize(size_t(n + 1));
   d.dexp_off.resize(size_t(n + 1));
-  k_partition<<<1, kMaxRanks + 1, 0, s>>>(c.S[0].nrow.p, c.S[0].trow.p, has1 ? c.S[1].nrow.p : nullptr,
-                                          has1 ? c.S[1].trow.p : nullptr, c.NB, n, d.dbounds.p);
-  YS_LAUNCH_CHECK();
+  // the partition is the static one (ctx_dist_static_plan), fixed across
+  // Newton iterations
+  ctx_dist_static_plan(c);
+  YS_CUDA(cudaMemcpyAsync(d.dbounds.p, d.sbounds.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
   d.need.resize(size_t(c.NB));
   YS_CUDA(cudaMemsetAsync(d.need.p, 0, size_t(c.NB), s));
   for (int w = 0; w < (has1 ? 2 : 1); ++w) {
@@ -437,7 +438,74 @@ void build_plan(Context& c) {
     d.max_rows = std::max(d.max_rows, d.bounds[k + 1] - d.bounds[k]);
   }
 }
+
+// Instance i of a 4-vertex stencil energy touches rows [r0, r1) (uniform 3x3).
+__global__ void k_flag_owned(const int4* __restrict__ conn, int64_t n, int32_t startP, int64_t r0, int64_t r1,
+                             uint8_t* __restrict__ flag) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int4 v = conn[i];
+  const int vv[4] = {v.x, v.y, v.z, v.w};
+  bool t = false;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int64_t R = (int64_t(startP) + 3 * int64_t(vv[l])) / 3;
+    t = t || (R >= r0 && R < r1);
+  }
+  flag[i] = t ? 1 : 0;
+}
 }  // namespace
+
+// Partition from the static structure's entry counts (the same weights as the
+// per-solve plan: entries per block row + 1), and per static SNH / bending
+// energy the instances touching this rank's rows.  Computed once per context.
+void ctx_dist_static_plan(Context& c) {
+  DistState& d = c.dist;
+  if (d.have_static) return;
+  const int n = d.nranks;
+  cudaStream_t s = c.stream;
+  if (!(c.uniform3 && c.S[0].all33)) fail(YS_ERR_VALIDATION, "distributed PCG supports uniform 3x3 block systems only");
+  d.dbounds.resize(size_t(n + 1));
+  k_partition<<<1, kMaxRanks + 1, 0, s>>>(c.S[0].nrow.p, c.S[0].trow.p, nullptr, nullptr, c.NB, n, d.dbounds.p);
+  YS_LAUNCH_CHECK();
+  d.sbounds.assign(size_t(n + 1), 0);
+  YS_CUDA(cudaMemcpyAsync(d.sbounds.data(), d.dbounds.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+  YS_CUDA(cudaStreamSynchronize(s));
+  const int64_t r0 = d.sbounds[d.rank], r1 = d.sbounds[d.rank + 1];
+  d.sel.clear();
+  d.sel.resize(c.energies.size());
+  d.nsel_e.assign(c.energies.size(), -1);
+  d.eval_owned = d.eval_total = 0;
+  DevBuf<uint8_t> flag;
+  DevBuf<int32_t> cnt;
+  cnt.resize(1);
+  for (size_t id = 0; id < c.energies.size(); ++id) {
+    const Energy& e = c.energies[id];
+    if (e.dynamic || !(e.kind == K_SNH || e.kind == K_BENDING) || e.n == 0) continue;
+    flag.resize(size_t(e.n));
+    const int32_t startP = e.target >= 0 ? int32_t(c.targets[e.target].start) : 0;
+    k_flag_owned<<<blocks_for(e.n), kTB, 0, s>>>(reinterpret_cast<const int4*>(e.conn.p), e.n, startP, r0, r1, flag.p);
+    YS_LAUNCH_CHECK();
+    d.sel[id].resize(size_t(e.n) + 1);
+    size_t tmp = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    YS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag.p, d.sel[id].p, cnt.p, int(e.n), s));
+    c.cubtmp.resize(std::max(c.cubtmp.n, tmp + 1));
+    YS_CUDA(cub::DeviceSelect::Flagged(c.cubtmp.p, tmp, it, flag.p, d.sel[id].p, cnt.p, int(e.n), s));
+    int32_t h = 0;
+    YS_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+    d.nsel_e[id] = h;
+    d.eval_owned += h;
+    d.eval_total += e.n;
+  }
+  // instances outside the subset are never evaluated while the partition is
+  // active: their contributions read as zero (non-owned rows are neither
+  // solved nor checked)
+  c.S[0].hcontrib.zero(s);
+  c.S[0].gcontrib.zero(s);
+  d.have_static = true;
+}
 
 void ctx_dist_unique_id(unsigned char* id) {
   ncclUniqueId u;
@@ -460,6 +528,7 @@ void ctx_dist_finalize(Context& c) {
   if (c.dist.kind == 2 && c.dist.nccl) nccl().CommDestroy(reinterpret_cast<ncclComm_t>(c.dist.nccl));
   c.dist.nccl = nullptr;
   c.dist.kind = 0;
+  c.dist.have_static = false;  // a new rank count recomputes the partition
 }
 
 void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats) {

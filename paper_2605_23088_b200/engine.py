@@ -422,8 +422,13 @@ class Engine:
         halo, exp = C.c_int64(), C.c_int64()
         self._c(self.f["dist_info"](self.ctx, C.byref(rank), C.byref(nranks), bounds.ctypes.data_as(_lib._PI64),
                                     C.byref(halo), C.byref(exp)))
-        return {"rank": rank.value, "nranks": nranks.value, "bounds": bounds[:nranks.value + 1].copy(),
-                "halo_rows": halo.value, "export_rows": exp.value}
+        out = {"rank": rank.value, "nranks": nranks.value, "bounds": bounds[:nranks.value + 1].copy(),
+               "halo_rows": halo.value, "export_rows": exp.value}
+        if "dist_eval_counts" in self.f:
+            ev, tot = C.c_int64(), C.c_int64()
+            self._c(self.f["dist_eval_counts"](self.ctx, C.byref(ev), C.byref(tot)))
+            out["eval_instances"], out["eval_total"] = ev.value, tot.value
+        return out
 
     def split_per_target(self, flat: np.ndarray) -> list[np.ndarray]:
         out, off = [], 0
