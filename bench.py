@@ -164,7 +164,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -466,7 +466,7 @@ def main():
         "assembly_roofline": {"bound": "hbm", "achieved": asm_gbs, "peak": peak, "unit": "GB/s",
                               "frac": asm_gbs / peak, "algorithmic_bytes": asm_bytes, "avg_ms": asm_ms},
         "eval_ms": eval_ms,
-        "eval_roofline": {"bound": "fp64", "kernel": "k_eval_* (pass A: gradient + H_D + Cholesky test; pass B: 9x9 Jacobi of the indefinite elements; point terms)",
+        "eval_roofline": {"bound": "fp64", "kernel": "k_eval_* (pass A: gradient + H_D + Cholesky test; pass B: clamped-eigenpair projection of the indefinite 9x9 elements, Jacobi fallback; point terms)",
                           "achieved": (eval_flops / (eval_ms * 1e-3) / 1e12) if eval_flops else None,
                           "peak": fp64_peak, "unit": "TFLOP/s",
                           "frac": (eval_flops / (eval_ms * 1e-3) / 1e12 / fp64_peak) if eval_flops else None,
