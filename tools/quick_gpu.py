@@ -4,21 +4,19 @@ import time
 
 import numpy as np
 
-from paper_2605_23088_b200 import configs
-from paper_2605_23088_b200.scene import SimConfig, Simulation
+import os
 
-simulation = lambda cfg, backend: Simulation(cfg)  # noqa: E731  (the B200 library)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import prepare  # noqa: E402
 
+state = os.environ.get("STATE", "rollout")
 names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
 for name in names:
     t0 = time.perf_counter()
-    cfg = SimConfig.from_dict(configs.CONFIGS[name]())
-    sim = simulation(cfg, "gpu")
+    sim = prepare(name, True, "gpu", state=state)
+    cfg = sim.config
     t1 = time.perf_counter()
-    sp = 0.1 * (0.025 if name == "c1" else 0.01)
-    configs.jitter_targets(sim, sp)
-    sim.begin_frame()
-    n = sim.refresh_dynamic_pairs()
+    n = sim.pair_count()
     t2 = time.perf_counter()
     eng = sim.eng
     eng.set_profiling(True)
