@@ -95,6 +95,26 @@ struct VertexBlockWriter {
   __device__ __forceinline__ void operator()(int pair, int k, int kk, double v) const {
     h[pair * 9 + (((swap >> pair) & 1u) ? kk * 3 + k : k * 3 + kk)] = v;
   }
+  // a whole 3x3 block (row-major v): four 16-byte stores and one 8-byte store
+  // (the block's 72 bytes start 16-byte aligned for every other pair)
+  __device__ __forceinline__ void block(int pair, const double (&v)[9]) const {
+    const bool sw = (swap >> pair) & 1u;
+    double o[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) o[k * 3 + kk] = sw ? v[kk * 3 + k] : v[k * 3 + kk];
+    double* d = h + pair * 9;
+    if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) *reinterpret_cast<double2*>(d + q) = make_double2(o[q], o[q + 1]);
+      d[8] = o[8];
+    } else {
+      d[0] = o[0];
+#pragma unroll
+      for (int q = 1; q < 9; q += 2) *reinterpret_cast<double2*>(d + q) = make_double2(o[q], o[q + 1]);
+    }
+  }
 };
 
 __device__ __forceinline__ uint32_t vertex_pair_swaps(const int32_t gs[4]) {

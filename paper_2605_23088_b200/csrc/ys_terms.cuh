@@ -564,6 +564,7 @@ __device__ __forceinline__ void expand_vb(const double* hd, const Writer& wr) {
     for (int b = 0; b < 4; ++b) {
       if (b < a) continue;
       const int pair = a * 4 - (a * (a - 1)) / 2 + (b - a);
+      double blk[9];
 #pragma unroll
       for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -579,9 +580,10 @@ __device__ __forceinline__ void expand_vb(const double* hd, const Writer& wr) {
               if (ea == 0.0 || eb == 0.0) continue;
               acc += ea * eb * hd[pk9(3 * i + k, 3 * ip + kk)];
             }
-          wr(pair, k, kk, acc);
-          if (a == b && kk != k) wr(pair, kk, k, acc);
+          blk[k * 3 + kk] = acc;
+          if (a == b && kk != k) blk[kk * 3 + k] = acc;
         }
+      wr.block(pair, blk);
     }
 }
 
