@@ -185,13 +185,11 @@ __global__ void __launch_bounds__(128) k_eval_stencil_a(EnergyDev E, const doubl
   if (full) edge_to_projection_space(hd);
   // M goes to the element's slot first; the positive-definiteness test then
   // factors the registers in place (no second 45-register copy)
-  double* m = mbuf + 45 * i;
-#pragma unroll
-  for (int q = 0; q < 45; ++q) m[q] = hd[q];
+  double* m = mbuf + kMStride * i;
+  store_m(m, hd);
   if (cholesky_pd9_inplace(hd)) {
     // M is PD: the projection is M itself (reloaded from its slot)
-#pragma unroll
-    for (int q = 0; q < 45; ++q) hd[q] = ld_reload(m + q);
+    reload_m(m, hd);
     expand_vertex_blocks(hd, full, wr);
     return;
   }
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(kProjStride, 3) k_eval_stencil_b_tri(const __g
     const int64_t slot = B.base[j] + (k - prej);
     const int64_t i = list[slot];
     double m[45];
-    if (force_fallback || !psd_project9_tri(mbuf + 45 * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
+    if (force_fallback || !psd_project9_tri(mbuf + kMStride * (B.base[j] + i), m, sm_proj + threadIdx.x, gsc, gstride)) {
       const unsigned f = atomicAdd(B.fbcount[j], 1u);
       B.fblist[j][f] = int32_t(i);
       continue;
@@ -279,9 +277,9 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_fallback(const __grid_co
     const EnergyDev& E = B.e[j];
     const int64_t i = B.fblist[j][k - pre[j]];  // element id
     double m[45];
-    const double* src = mbuf + 45 * (B.base[j] + i);
+    const double* src = mbuf + kMStride * (B.base[j] + i);
 #pragma unroll
-    for (int q = 0; q < 45; ++q) m[q] = src[q];
+    for (int q = 0; q < 45; ++q) m[q] = src[q];  // (fallback paths: scalar loads)
     psd_project9(m);
     const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
     const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
@@ -308,9 +306,9 @@ __global__ void __launch_bounds__(128) k_eval_stencil_b_batch(const __grid_const
     const int64_t slot = B.base[j] + (k - pre[j]);
     const int64_t i = list[slot];
     double m[45];
-    const double* src = mbuf + 45 * (B.base[j] + i);
+    const double* src = mbuf + kMStride * (B.base[j] + i);
 #pragma unroll
-    for (int q = 0; q < 45; ++q) m[q] = src[q];
+    for (int q = 0; q < 45; ++q) m[q] = src[q];  // (fallback paths: scalar loads)
     psd_project9(m);
     const int4 v = reinterpret_cast<const int4*>(E.conn)[i];
     const int32_t gs[4] = {E.startP + 3 * v.x, E.startP + 3 * v.y, E.startP + 3 * v.z, E.startP + 3 * v.w};
@@ -998,7 +996,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
       evd_total += e.n;
     }
   }
-  c.evd_m.resize(std::max(c.evd_m.n, size_t(45 * evd_total)));
+  c.evd_m.resize(std::max(c.evd_m.n, size_t(kMStride * evd_total)));
   c.evd_list.resize(std::max(c.evd_list.n, size_t(evd_total)));
   c.evd_fblist.resize(std::max(c.evd_fblist.n, size_t(evd_total)));
   const bool pass_b = with_hessian && project;
@@ -1077,7 +1075,7 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
         unsigned int* cnt = c.evd_count.p + id;
         const unsigned ga = grid_for(e.n, 128);
         int32_t* lst = c.evd_list.p + evd_base[id];
-        double* mb = c.evd_m.p + 45 * evd_base[id];
+        double* mb = c.evd_m.p + kMStride * evd_base[id];
         const int kind = e.kind == K_SNH ? 0 : 1;
         // distributed solve: only the instances touching this rank's rows
         const bool part_sel = c.dist.kind && c.dist.nranks > 1 && c.dist.have_static &&

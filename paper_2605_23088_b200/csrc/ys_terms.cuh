@@ -200,6 +200,38 @@ __device__ __forceinline__ double ld_reload(const double* p) {
   asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ double2 ld_reload2(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// The 9x9 M of an element (packed 45) in its slot of the pass-B buffer: a
+// 46-double stride keeps every slot 16-byte aligned (23 vector accesses).
+constexpr int kMStride = 46;
+__device__ __forceinline__ void store_m(double* m, const double* a) {
+#pragma unroll
+  for (int q = 0; q < 44; q += 2) *reinterpret_cast<double2*>(m + q) = make_double2(a[q], a[q + 1]);
+  m[44] = a[44];
+}
+__device__ __forceinline__ void load_m(const double* __restrict__ m, double* a) {
+#pragma unroll
+  for (int q = 0; q < 44; q += 2) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(m + q));
+    a[q] = v.x;
+    a[q + 1] = v.y;
+  }
+  a[44] = __ldg(m + 44);
+}
+__device__ __forceinline__ void reload_m(const double* m, double* a) {
+#pragma unroll
+  for (int q = 0; q < 44; q += 2) {
+    const double2 v = ld_reload2(m + q);
+    a[q] = v.x;
+    a[q + 1] = v.y;
+  }
+  a[44] = ld_reload(m + 44);
+}
 constexpr int kProjSlots = 53;  // shared: [0, 36) the used vectors (T basis), [36, 45) d, [45, 53) e
 constexpr int kSlotD = 36, kSlotE = 45;
 constexpr int kProjScratch = 42;  // global, per thread: [0, 35) reflectors v_k, [35, 42) beta_k
@@ -212,8 +244,7 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
   auto G = [&](int slot) -> double& { return gsc[slot * gstride]; };
   double a[45];
   double n2 = 0.0;
-#pragma unroll
-  for (int q = 0; q < 45; ++q) a[q] = msrc[q];
+  load_m(msrc, a);
 #pragma unroll
   for (int i = 0; i < 9; ++i)
 #pragma unroll
@@ -398,8 +429,7 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
     if (cnt != kneg) return false;
   }
   if (kneg == 0) {
-#pragma unroll
-    for (int q = 0; q < 45; ++q) P[q] = ld_reload(msrc + q);
+    reload_m(msrc, P);
     return true;
   }
   // ---- 4. eigenvectors of T for the used eigenvalues (T basis, smem slots
