@@ -19,12 +19,12 @@ from paper_2605_23088_b200.scene import SimConfig  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def _assembled(backend, name, mode=None):
+def _assembled(backend, name, mode=None, jitter=None):
     cfg = SimConfig.from_dict(configs.CONFIGS[name]())
     sim = simulation(cfg, backend)
     if mode is not None:
         sim.eng.set_option("eval_evd", mode)
-    configs.jitter_targets(sim, 0.002 if name == "c3" else 0.001)
+    configs.jitter_targets(sim, jitter if jitter is not None else (0.002 if name == "c3" else 0.001))
     sim.begin_frame()
     sim.refresh_dynamic_pairs()
     sim.eng.refresh_dynamic()
@@ -46,3 +46,15 @@ def test_projection_paths_agree(name):
     assert rel(ht, hj) <= 1e-12 and rel(hf, hj) <= 1e-12
     for h in (ht, hj, hf):
         assert rel(h, ho) <= 1e-9
+
+
+def test_projection_paths_under_strong_distortion():
+    """C2 with a jitter of half the cell size: inverted and strongly sheared tets,
+    up to nine negative eigenvalues (the positive-side path) and near-degenerate
+    spectra (fallbacks allowed); every path within 1e-9 of the oracle."""
+    ho, _, _ = _assembled("oracle", "c2", jitter=0.005)
+    ht, nt, ft = _assembled("gpu", "c2", 1, jitter=0.005)
+    hj, _, _ = _assembled("gpu", "c2", 0, jitter=0.005)
+    assert nt > 0 and ft <= nt // 100
+    assert rel(ht, hj) <= 1e-11
+    assert rel(ht, ho) <= 1e-9 and rel(hj, ho) <= 1e-9
