@@ -308,8 +308,11 @@ int ys_stream(ys_context* ctx, void** stream);
  * stages sequentially (bitwise the same step).  "eval_evd" (default 1) projects
  * the indefinite 9x9 element Hessians by the clamped-eigenpair path
  * (tridiagonal QL + inverse iteration, verified; failures go to the Jacobi
- * EVD); 0 sends every element through the Jacobi EVD (both within 1e-12 of
- * the exact projection). */
+ * EVD); 0 sends every element through the Jacobi EVD, 2 hands every element
+ * to the fallback kernel (all within 1e-12 of the exact projection).
+ * "pcg_copy" (default 1) solves uniform 3x3 systems over the sliced-ELL copy;
+ * 0 takes the row-gather persistent kernel (the path used when the copy's
+ * plan does not fit shared memory; tests). */
 int ys_set_option(ys_context* ctx, const char* name, int64_t value);
 /* Times one kernel class alone: reps launches bracketed by CUDA events on the
  * context stream.  which: 0 = SpMV row gather from upper storage (static +

@@ -1305,6 +1305,7 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
   return guarded(c, [&] {
     const std::string n = name ? name : "";
     if (n == "overlap") c->overlap = value != 0;
+    else if (n == "pcg_copy") c->pcg_copy = value != 0;
     else if (n == "eval_evd") {
       if (value < 0 || value > 2)
         fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi), 1 (clamped eigenpairs) or 2 (every element through the fallback)");

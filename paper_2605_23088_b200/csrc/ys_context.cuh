@@ -278,6 +278,7 @@ struct Context {
   // profiling
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
+  bool pcg_copy = true;  // uniform 3x3 solve over the sliced-ELL copy (false: the row-gather kernel; tests)
   int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only,
                        // 2 every element handed to the fallback list (tests)
   double stage_ms[8] = {0};

@@ -1146,8 +1146,8 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
       bool launched = false;
       c.gridbar.resize(sizeof(GridBar));
       GridBar* gbp = reinterpret_cast<GridBar*>(c.gridbar.p);
-      if (!launched) {
-        YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
+      YS_CUDA(cudaMemsetAsync(c.gridbar.p, 0, sizeof(GridBar), s));
+      if (!launched && c.pcg_copy) {
         // full sliced-ELL copy, per-warp plan cache in shared memory
         sell_build(c, 4);
         SellDev sl = sell_dev(c);

@@ -344,3 +344,32 @@ def test_overlap_and_sequential_steps_are_bitwise_equal(name):
         st = sim.eng.minimize_step(1e-4)
         outs.append((hashlib.sha256(np.ascontiguousarray(st.dx).tobytes()).hexdigest(), st.pcg_iterations))
     assert outs[0] == outs[1], outs
+
+
+@pytest.mark.parametrize("name", ["c2"])
+def test_row_gather_pcg_path(name):
+    """The uniform-3x3 solve's second kernel (row gather from upper storage, the
+    path taken when the sliced-ELL copy's plan does not fit shared memory),
+    forced with ys_set_option("pcg_copy", 0): the oracle's iteration count and
+    dx within 1e-9, and the path is reported."""
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig
+    from backends import simulation
+
+    def step(backend, copy=None):
+        sim = simulation(SimConfig.from_dict(configs.CONFIGS[name]()), backend)
+        if copy is not None:
+            sim.eng.set_option("pcg_copy", copy)
+        configs.jitter_targets(sim, 0.001)
+        sim.begin_frame()
+        sim.refresh_dynamic_pairs()
+        st = sim.eng.minimize_step(1e-4)
+        path = sim.eng.pcg_path() if backend == "gpu" else None
+        sim.eng.close()
+        return st, path
+
+    so, _ = step("oracle")
+    sg, pg = step("gpu", 0)
+    assert pg == "row gather"
+    assert sg.pcg_iterations == so.pcg_iterations
+    assert np.max(np.abs(sg.dx - so.dx)) <= 1e-9 * np.max(np.abs(so.dx))
