@@ -6,12 +6,13 @@
 // for the vector work).  Per iteration (same recurrence as pcg,
 // solver.cpp:151-200):
 //
-//   halo     pack this rank's export rows of p -> allgather -> unpack the
-//            other ranks' export rows into p        (1 exchange)
-//   SpMV     hp = H p on owned rows (the 4-lane row gather of ys_spmv.cuh);
+//   SpMV     hp = H p on owned rows (sliced-ELL copy of the owned rows);
 //            pHp rank partial                      -> allgather -> alpha
-//   update   x, r, z on owned rows; r.r, r.z       -> allgather -> rel, beta
-//   p        p = z + beta p on owned rows
+//   update   x, r, z on owned rows; r.r, r.z partials plus z and the
+//            pre-update p of the export rows       -> allgather -> rel, beta
+//   p        p = z + beta p on owned rows, and on the halo rows from the
+//            received z and p (the owner's formula: bitwise the owner's p)
+// (the initial p halo is exchanged once before the loop).
 //
 // Every rank sums the gathered partials in rank order, so alpha / beta /
 // status are bit-identical on all ranks and the loop ends on the same
@@ -166,6 +167,38 @@ __global__ void k_unpack(const double* __restrict__ recv, const int32_t* __restr
   p[3 * int64_t(exp[e]) + j % 3] = recv[(int64_t(k) * maxc + (e - exp_off[k])) * 3 + j % 3];
 }
 
+// Fused exchange: after the update phase each rank sends, in one allgather,
+// its r.r / r.z partials, z and the pre-update p of its export rows; every
+// receiver forms the halo p = z + beta p itself (the owner's formula and
+// operands: bitwise the owner's value), so the p halo needs no exchange of
+// its own.  Send layout: [2 partials][3 max_exp z][3 max_exp p].
+__global__ void k_pack_zp(const double* __restrict__ z, const double* __restrict__ p,
+                          const int32_t* __restrict__ exp, int64_t cnt, int64_t maxc, double* __restrict__ send,
+                          const PcgState* st) {
+  if (st->status) return;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= 3 * cnt) return;
+  const int64_t g = 3 * int64_t(exp[i / 3]) + i % 3;
+  send[2 + i] = z[g];
+  send[2 + 3 * maxc + i] = p[g];
+}
+
+__global__ void k_unpack_zp(const double* __restrict__ recv, const int32_t* __restrict__ exp,
+                            const int64_t* __restrict__ exp_off, int n, int me, int64_t maxc, int64_t total,
+                            double* __restrict__ p, const PcgState* st) {
+  if (st->status) return;
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= 3 * total) return;
+  const int64_t e = j / 3;
+  const int k = owner_of(exp_off, n, e);
+  if (k == me) return;
+  const double* rk = recv + int64_t(k) * (2 + 6 * maxc);
+  const int64_t q = (e - exp_off[k]) * 3 + j % 3;
+  const double b = st->beta;
+  const double zz = rk[2 + q], pp = rk[2 + 3 * maxc + q];
+  p[3 * int64_t(exp[e]) + j % 3] = zz + b * pp;
+}
+
 // x slices of every rank -> the full vector (rank k's rows at slot k).
 __global__ void k_gather_rows(const double* __restrict__ recv, const int64_t* __restrict__ bounds, int n,
                               int64_t maxr, int64_t nb, double* __restrict__ x) {
@@ -260,12 +293,12 @@ __global__ void k_dinit(const double* __restrict__ g, const double* __restrict__
 
 // Rank-ordered sums of the gathered partials (identical on every rank).
 template <int K>
-__device__ __forceinline__ void rank_sums(const double* all, int n, double (&t)[K]) {
+__device__ __forceinline__ void rank_sums(const double* all, int n, double (&t)[K], int64_t stride = K) {
 #pragma unroll
   for (int k = 0; k < K; ++k) t[k] = 0.0;
   for (int q = 0; q < n; ++q)
 #pragma unroll
-    for (int k = 0; k < K; ++k) t[k] += all[q * K + k];
+    for (int k = 0; k < K; ++k) t[k] += all[q * stride + k];
 }
 
 __global__ void k_dinit_fin(PcgState* st, const double* all, int n, double* hist) {
@@ -344,10 +377,10 @@ __global__ void __launch_bounds__(kTB) k_dupdate(const double* __restrict__ minv
 }
 
 // rel, history, convergence test, beta (solver.cpp:183-197).
-__global__ void k_dbeta(PcgState* st, const double* all, int n, double* hist) {
+__global__ void k_dbeta(PcgState* st, const double* all, int n, double* hist, int64_t stride) {
   if (st->status) return;
   double t[2];
-  rank_sums<2>(all, n, t);
+  rank_sums<2>(all, n, t, stride);
   const long long it = st->it;
   const double rel = sqrt(t[0]) / st->gnorm;
   st->it = it + 1;
@@ -553,8 +586,9 @@ void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats
   c.partials.resize(std::max<size_t>(c.partials.n, size_t(2 * grid)));
   const int64_t hist_cap = std::min<int64_t>(max_iter, int64_t(1) << 22) + 2;
   c.hist.resize(std::max<size_t>(c.hist.n, size_t(hist_cap)));
-  d.send.resize(size_t(3 * std::max(d.max_exp, d.max_rows) + 1));
-  d.recv.resize(size_t(3 * std::max(d.max_exp, d.max_rows) * n + 1));
+  const int64_t zp = 2 + 6 * d.max_exp;  // fused exchange record per rank
+  d.send.resize(size_t(std::max(3 * std::max(d.max_exp, d.max_rows), zp) + 1));
+  d.recv.resize(size_t(std::max(3 * std::max(d.max_exp, d.max_rows), zp) * n + 1));
   d.dsend.resize(2);
   d.dall.resize(size_t(2 * n));
 
@@ -582,22 +616,33 @@ void ctx_dist_pcg(Context& c, double tol, int64_t max_iter, ys_step_stats* stats
   }
   const int sg = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(32 * sl.nslices, kTB),
                                                             int64_t(occ_sell) * sm_count())));
+  // the initial p (= z) halo; afterwards it travels with the update's partials
+  if (d.max_exp > 0) {
+    k_pack<<<blocks_for(3 * my_exp), kTB, 0, s>>>(c.p.p, d.exp.p + d.exp_off[me], my_exp, d.send.p, st);
+    allgather(c, d.send.p, d.recv.p, 3 * d.max_exp);
+    k_unpack<<<blocks_for(3 * total_exp), kTB, 0, s>>>(d.recv.p, d.exp.p, d.dexp_off.p, n, me, d.max_exp, total_exp,
+                                                       c.p.p, st);
+    YS_LAUNCH_CHECK();
+  }
+  // Two allgathers per iteration: pHp partials; then the r.r / r.z partials
+  // together with z and the pre-update p of the export rows (k_pack_zp /
+  // k_unpack_zp: the receivers update their halo p themselves).
   auto iteration = [&] {
-    if (d.max_exp > 0) {
-      k_pack<<<blocks_for(3 * my_exp), kTB, 0, s>>>(c.p.p, d.exp.p + d.exp_off[me], my_exp, d.send.p, st);
-      allgather(c, d.send.p, d.recv.p, 3 * d.max_exp);
-      k_unpack<<<blocks_for(3 * total_exp), kTB, 0, s>>>(d.recv.p, d.exp.p, d.dexp_off.p, n, me, d.max_exp, total_exp,
-                                                         c.p.p, st);
-    }
     k_dspmv_sell<<<sg, kTB, 0, s>>>(sl, c.p.p, c.hp.p, st, part, d.dsend.p);
     allgather(c, d.dsend.p, d.dall.p, 1);
     k_dalpha<<<1, 1, 0, s>>>(st, d.dall.p, n);
-    k_dupdate<<<vg, kTB, 0, s>>>(c.minv.p, c.DX.p, c.r.p, c.z.p, c.p.p, c.hp.p, r0, r1, st, part, d.dsend.p);
-    allgather(c, d.dsend.p, d.dall.p, 2);
-    k_dbeta<<<1, 1, 0, s>>>(st, d.dall.p, n, c.hist.p);
+    k_dupdate<<<vg, kTB, 0, s>>>(c.minv.p, c.DX.p, c.r.p, c.z.p, c.p.p, c.hp.p, r0, r1, st, part, d.send.p);
+    if (d.max_exp > 0)
+      k_pack_zp<<<blocks_for(3 * my_exp), kTB, 0, s>>>(c.z.p, c.p.p, d.exp.p + d.exp_off[me], my_exp, d.max_exp,
+                                                        d.send.p, st);
+    allgather(c, d.send.p, d.recv.p, zp);
+    k_dbeta<<<1, 1, 0, s>>>(st, d.recv.p, n, c.hist.p, zp);
     k_dpupdate<<<vg, kTB, 0, s>>>(c.z.p, c.p.p, r0, r1, st);
+    if (d.max_exp > 0)
+      k_unpack_zp<<<blocks_for(3 * total_exp), kTB, 0, s>>>(d.recv.p, d.exp.p, d.dexp_off.p, n, me, d.max_exp,
+                                                             total_exp, c.p.p, st);
     YS_LAUNCH_CHECK();
-    c.launches += 7 + (d.max_exp > 0 ? 2 : 0);
+    c.launches += 6 + (d.max_exp > 0 ? 2 : 0);
   };
   // Status is identical on every rank, so every rank leaves after the same chunk.
   const int chunk = d.kind == 2 ? 8 : 1;
