@@ -18,6 +18,7 @@
 //      DiagAccumulator block (static H block + dynamic contributions one by
 //      one) and inverts it for the preconditioner.
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -1032,14 +1033,17 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
       YS_LAUNCH_CHECK();
       ++c.launches;
     } else {
-      static bool attr = false;
+      // the dynamic shared-memory opt-in is per device (a process may hold
+      // contexts on several devices)
+      static std::atomic<uint64_t> attr_devices{0};
       const size_t smem = size_t(kProjSlots) * kProjStride * sizeof(double);
-      if (!attr) {
+      const uint64_t bit = uint64_t(1) << (c.device & 63);
+      if (!(attr_devices.load() & bit)) {
         YS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_eval_stencil_b_tri<0>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         YS_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_eval_stencil_b_tri<1>),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = true;
+        attr_devices.fetch_or(bit);
       }
       const unsigned gt = unsigned(sm_count() * 3);
       // per-thread reflector scratch; the two static-evaluation streams get
