@@ -352,6 +352,9 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
         double g = dm - dl + 2.0 * el * el / (h + copysign(rh, h));
         double r;
         double s = 1.0, c = 1.0, pp = 0.0;
+        // the lowest block start among the lanes sweeping together: steps below
+        // it are idle for every lane (one reduction per sweep, uniform break)
+        const int lmin = __reduce_min_sync(__activemask(), l);
 #pragma unroll
         for (int i = 7; i >= 0; --i) {
           if (i < m && i >= l) {
@@ -369,7 +372,7 @@ __device__ __forceinline__ bool psd_project9_tri(const double* __restrict__ msrc
             lam[i + 1] = g + pp;
             g = c * r - b;
           }
-          if (i > 0 && !__any_sync(__activemask(), i - 1 >= l)) break;
+          if (i - 1 < lmin) break;
         }
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
