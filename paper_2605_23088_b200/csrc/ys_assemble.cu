@@ -709,6 +709,21 @@ __global__ void k_gather_h(const int64_t* __restrict__ seg, const uint32_t* __re
   values[voff[u] + e] = acc;
 }
 
+// The same over a selection of unique blocks (the distributed solve's owned
+// rows).
+__global__ void k_gather_h_sel(const int64_t* __restrict__ seg, const uint32_t* __restrict__ perm,
+                               const double* __restrict__ hc, const int32_t* __restrict__ sel, int64_t nsel, int rc,
+                               const int64_t* __restrict__ voff, double* __restrict__ values) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nsel * rc) return;
+  const int64_t u = sel[t / rc];
+  const int e = int(t % rc);
+  const int64_t j0 = seg[u], j1 = seg[u + 1];
+  double acc = 0.0;
+  for (int64_t j = j0; j < j1; ++j) acc += hc[perm[j] + e];
+  values[voff[u] + e] = acc;
+}
+
 struct GroupView {
   const int32_t* gseg;
   const uint32_t* gperm;
@@ -888,10 +903,10 @@ __device__ __forceinline__ void block_row_work(int64_t b, const BlocksDev& B, co
 // blocks of a uniform layout).
 template <int N>
 __global__ void k_block_rows(BlocksDev B, const int32_t* __restrict__ list, int64_t nb, GroupView S0, GroupView S1,
-                             double* G, double* diag, double* minv, int32_t* bflag, int want_h) {
+                             double* G, double* diag, double* minv, int32_t* bflag, int want_h, int64_t b0 = 0) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= nb) return;
-  const int64_t b = list ? list[q] : q;
+  const int64_t b = list ? list[q] : b0 + q;
   block_row_work<N>(b, B, S0, S1, G, diag, minv, bflag, want_h);
 }
 
@@ -1191,10 +1206,22 @@ void ctx_gather_all(Context& c, int only, cudaStream_t s) {
   for (int w = 0; w < 2; ++w) {
     if (only >= 0 && w != only) continue;
     Structure& st = c.S[w];
-    for (auto& g : st.groups) {
+    const bool dsel = w == 0 && c.dist.kind && c.dist.nranks > 1 && c.dist.have_static &&
+                      c.dist.ngsel.size() == st.groups.size();
+    for (size_t gi = 0; gi < st.groups.size(); ++gi) {
+      const auto& g = st.groups[gi];
       const int rc = int(g[0] * g[1]);
       const int64_t cnt = g[3];
       if (cnt == 0) continue;
+      if (dsel) {  // only the blocks touching this rank's rows
+        const int64_t ns = c.dist.ngsel[gi];
+        if (ns > 0)
+          k_gather_h_sel<<<grid_for(ns * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, c.dist.gsel[gi].p, ns,
+                                                           rc, st.voff.p, st.values.p);
+        YS_LAUNCH_CHECK();
+        ++c.launches;
+        continue;
+      }
       k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc, st.voff.p,
                                                     st.values.p);
       YS_LAUNCH_CHECK();
@@ -1232,9 +1259,13 @@ void ctx_block_rows(Context& c, bool want_h) {
   const BlocksDev B = blocks_view(c);
   const GroupView S0 = group_view(c.S[0], true), S1 = group_view(c.S[1], true);
   const int wh = want_h ? 1 : 0;
+  // distributed solve (uniform 3x3 only): the rank's rows [b0, b0 + nb)
+  const bool own = c.dist.kind && c.dist.nranks > 1 && c.dist.have_static && c.rc_classes.size() == 1;
+  const int64_t b0 = own ? c.dist.sbounds[size_t(c.dist.rank)] : 0;
   for (size_t k = 0; k < c.rc_classes.size(); ++k) {
     const int32_t* list = c.rc_classes.size() == 1 ? nullptr : c.rc_lists[k].p;
-    const int64_t nb = c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[k].n);
+    const int64_t nb = own ? c.dist.sbounds[size_t(c.dist.rank) + 1] - b0
+                           : (c.rc_classes.size() == 1 ? c.NB : int64_t(c.rc_lists[k].n));
     if (nb == 0) continue;
     const unsigned g = grid_for(nb, 128);
     if (c.rc_classes[k] == 9 || c.rc_classes[k] == 12) {
@@ -1249,7 +1280,7 @@ void ctx_block_rows(Context& c, bool want_h) {
     }
 #define YS_ROWS(N)                                                                                            \
   case N:                                                                                                     \
-    k_block_rows<N><<<g, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh); \
+    k_block_rows<N><<<g, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh, b0); \
     break;
     switch (c.rc_classes[k]) {
       YS_ROWS(1)

@@ -187,6 +187,8 @@ struct DistState {
   std::vector<DevBuf<int32_t>> sel;           // per energy: selected instances (empty: all)
   std::vector<int64_t> nsel_e;                // per energy: count (-1: all)
   int64_t eval_owned = 0, eval_total = 0;     // static stencil instances evaluated / in the scene
+  std::vector<DevBuf<int32_t>> gsel;          // per static shape group: unique blocks touching owned rows
+  std::vector<int64_t> ngsel;
 };
 
 struct Context {

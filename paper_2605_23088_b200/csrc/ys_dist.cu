@@ -472,6 +472,15 @@ void build_plan(Context& c) {
   }
 }
 
+// Unique block u (DoF coordinates row/col) touches rows [r0, r1).
+__global__ void k_flag_owned_blocks(const int32_t* __restrict__ row, const int32_t* __restrict__ col, int64_t u0,
+                                    int64_t n, int64_t r0, int64_t r1, uint8_t* __restrict__ flag) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t R = row[u0 + t] / 3, C = col[u0 + t] / 3;
+  flag[t] = ((R >= r0 && R < r1) || (C >= r0 && C < r1)) ? 1 : 0;
+}
+
 // Instance i of a 4-vertex stencil energy touches rows [r0, r1) (uniform 3x3).
 __global__ void k_flag_owned(const int4* __restrict__ conn, int64_t n, int32_t startP, int64_t r0, int64_t r1,
                              uint8_t* __restrict__ flag) {
@@ -531,6 +540,30 @@ void ctx_dist_static_plan(Context& c) {
     d.nsel_e[id] = h;
     d.eval_owned += h;
     d.eval_total += e.n;
+  }
+  // the static group's unique blocks touching owned rows (the assembly gather
+  // of this rank)
+  const Structure& st0 = c.S[0];
+  d.gsel.clear();
+  d.gsel.resize(st0.groups.size());
+  d.ngsel.assign(st0.groups.size(), 0);
+  for (size_t gi = 0; gi < st0.groups.size(); ++gi) {
+    const auto& g = st0.groups[gi];
+    const int64_t u0 = g[2], gcnt = g[3];
+    if (gcnt == 0) continue;
+    flag.resize(size_t(gcnt));
+    k_flag_owned_blocks<<<blocks_for(gcnt), kTB, 0, s>>>(st0.row.p, st0.col.p, u0, gcnt, r0, r1, flag.p);
+    YS_LAUNCH_CHECK();
+    d.gsel[gi].resize(size_t(gcnt) + 1);
+    size_t tmp = 0;
+    cub::CountingInputIterator<int32_t> it(static_cast<int32_t>(u0));
+    YS_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flag.p, d.gsel[gi].p, cnt.p, int(gcnt), s));
+    c.cubtmp.resize(std::max(c.cubtmp.n, tmp + 1));
+    YS_CUDA(cub::DeviceSelect::Flagged(c.cubtmp.p, tmp, it, flag.p, d.gsel[gi].p, cnt.p, int(gcnt), s));
+    int32_t h = 0;
+    YS_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+    d.ngsel[gi] = h;
   }
   // instances outside the subset are never evaluated while the partition is
   // active: their contributions read as zero (non-owned rows are neither
