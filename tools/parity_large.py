@@ -24,7 +24,7 @@ t2 = time.time()
 print(f"{name}: build+pairs gpu {t1-t0:.1f}s oracle {t2-t1:.1f}s", flush=True)
 eg, eo = g.eng, o.eng
 pg, po = eg.get_pairs(g.contact_pairset), eo.get_pairs(o.contact_pairset)
-print("pairs", len(pg) // 2, "equal", np.array_equal(pg, po), flush=True)
+print("pairs", len(pg), "equal", np.array_equal(pg, po), flush=True)
 for e in (eg, eo):
     e.refresh_dynamic()
     e.assemble(True, True)
