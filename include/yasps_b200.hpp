@@ -118,6 +118,54 @@ class Engine {
     return id;
   }
 
+  // ---- contact beyond point-point (not in the reference) --------------------
+  int32_t add_stencil_set(int32_t union_id, int32_t arity, bool dynamic) {
+    int32_t id = -1;
+    check(ys_add_stencil_set(ctx_, union_id, arity, dynamic ? 1 : 0, &id));
+    return id;
+  }
+  // kind 1 PT (points, triangles), 2 EE (edges), 3 PE (points, edges); union-local point indices
+  void set_stencil_primitives(int32_t set, int32_t kind, const std::vector<int64_t>& a, int64_t arity_a,
+                              const std::vector<int64_t>& b = {}, int64_t arity_b = 1) {
+    check(ys_set_stencil_primitives(ctx_, set, kind, int64_t(a.size()) / arity_a, a.data(),
+                                    int64_t(b.size()) / arity_b, b.empty() ? nullptr : b.data()));
+  }
+  int64_t refresh_stencils(int32_t set, double dhat) {
+    int64_t n = 0;
+    check(ys_refresh_stencils(ctx_, set, dhat, &n));
+    return n;
+  }
+  int32_t add_point_triangle_barrier(int32_t set, double dhat, double kappa, double weight) {
+    int32_t id = -1;
+    check(ys_add_point_triangle_barrier(ctx_, set, dhat, kappa, weight, &id));
+    return id;
+  }
+  int32_t add_edge_edge_barrier(int32_t set, double dhat, double kappa, double weight) {
+    int32_t id = -1;
+    check(ys_add_edge_edge_barrier(ctx_, set, dhat, kappa, weight, &id));
+    return id;
+  }
+  int32_t add_point_edge_barrier(int32_t set, double dhat, double kappa, double weight) {
+    int32_t id = -1;
+    check(ys_add_point_edge_barrier(ctx_, set, dhat, kappa, weight, &id));
+    return id;
+  }
+
+  // ---- Simulation helpers on the device -------------------------------------
+  // refresh_dynamic_pairs (sim.cpp:456-484): the reference's pair list and order
+  int64_t refresh_pairs(int32_t pairset, double dhat, const std::vector<int32_t>& child_is_fixed = {}) {
+    int64_t n = 0;
+    check(ys_refresh_pairs(ctx_, pairset, dhat, child_is_fixed.empty() ? nullptr : child_is_fixed.data(), &n));
+    return n;
+  }
+  // X = X0 - alpha dx of the last minimize_step; returns |alpha dx|_inf (sim.cpp:545-562)
+  double step_targets(double alpha) {
+    double m = 0.0;
+    check(ys_step_targets(ctx_, alpha, &m));
+    return m;
+  }
+  void set_option(const char* name, int64_t value) { check(ys_set_option(ctx_, name, value)); }
+
   // ---- relsim::Engine members ---------------------------------------------
   void build() {  // Engine::Engine (engine.cpp:7-20)
     check(ys_finalize(ctx_));
