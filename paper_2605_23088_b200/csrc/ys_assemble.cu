@@ -1016,12 +1016,11 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
   c.evd_list.resize(std::max(c.evd_list.n, size_t(evd_total)));
   c.evd_fblist.resize(std::max(c.evd_fblist.n, size_t(evd_total)));
   const bool pass_b = with_hessian && project;
-  // pass B (Jacobi EVD of the indefinite elements) runs right after each
-  // energy's pass A, while its M buffer (360 B per indefinite element) sits in
-  // L2 (batching pass B over several bodies was measured slower: C5 eval stage
-  // per energy 4.93 ms, batches of 2 bodies 5.0, 4 bodies 5.4, all 8 6.4 ms);
-  // many small energies of one kind still share a launch.
-  constexpr int64_t kBatchElems = 1;
+  // pass B runs once per batch of up to kStencilBatch energies of one kind
+  // after their pass A (one grid-stride launch, no per-energy tails): with the
+  // clamped-eigenpair projection batching all C5 bodies is faster (eval 1.89
+  // -> 1.72 ms); round 1's Jacobi pass B lost L2 residency of M when batched.
+  constexpr int64_t kBatchElems = int64_t(1) << 40;
   const unsigned gb = unsigned(sm_count() * 4);
   std::vector<size_t> pending;
   int pending_kind = -1;
