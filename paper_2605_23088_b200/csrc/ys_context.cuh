@@ -288,8 +288,8 @@ struct Context {
   int64_t launches = 0;
   cudaEvent_t ev[10] = {};
   // second stream: the static energies' evaluation overlaps the dynamic rebuild
-  cudaStream_t stream2 = nullptr, stream3 = nullptr;  // stream3: the odd static energies
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join3 = nullptr;
+  cudaStream_t stream2 = nullptr;  // the static energies' evaluation and gather
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   DistState dist;
   ContactScratch contact;
