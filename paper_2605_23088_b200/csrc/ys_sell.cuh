@@ -100,20 +100,46 @@ __device__ __forceinline__ void sell_acc(const SellDev& S, int64_t slice, int la
   }
 }
 
+// PCG vectors kept in L2 across the solve's phases: loads / stores carrying an
+// L2::evict_last policy (the matrix copy streams with evict-first loads).
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_keep2(const double2* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_keep(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void load_vec3_keep(const double* p, double& x0, double& x1, double& x2, uint64_t pol) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
+  const double2 w0 = ld_keep2(w, pol), w1 = ld_keep2(w + 1, pol);
+  if (a & 8) {
+    x0 = w0.y; x1 = w1.x; x2 = w1.y;
+  } else {
+    x0 = w0.x; x1 = w0.y; x2 = w1.x;
+  }
+}
+
 // Same accumulation with the lane's column DoFs already in shared memory
 // (cols[j * 32 + lane], j < Lh) and its first entry row e0: the x gathers and
 // the value loads issue together.
 template <int H>
 __device__ __forceinline__ void sell_acc_cached(const SellDev& S, int64_t e0, const int32_t* cols, int Lh, int lane,
-                                                const double* x, double& a0, double& a1, double& a2) {
+                                                const double* x, double& a0, double& a1, double& a2, uint64_t pol) {
   for (int k = 0; k < Lh; k += 2) {
     const bool two = k + 1 < Lh;
     const int k2 = two ? k + 1 : k;
     const int64_t e1 = e0 + k, e2 = e0 + k2;
     const int32_t c1 = cols[k * 32 + lane], c2 = cols[k2 * 32 + lane];
     double x0, x1, x2, y0, y1, y2;
-    load_vec3(x + c1, x0, x1, x2);
-    load_vec3(x + c2, y0, y1, y2);
+    load_vec3_keep(x + c1, x0, x1, x2, pol);
+    load_vec3_keep(x + c2, y0, y1, y2, pol);
     const double2* v1 = reinterpret_cast<const double2*>(S.val + e1 * 288) + lane;
     const double2* v2 = reinterpret_cast<const double2*>(S.val + e2 * 288) + lane;
     const double2 p0 = __ldcs(v1), p1 = __ldcs(v1 + 32), p2 = __ldcs(v1 + 64), p3 = __ldcs(v1 + 96);

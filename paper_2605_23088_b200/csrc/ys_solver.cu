@@ -550,6 +550,7 @@ struct SellPhaseA {
   int32_t* cols;
   int kn, wl, grp, h, warp;
   int64_t gw, NW;
+  uint64_t pol;  // L2 evict_last for the vectors
 
   __device__ void prologue(double* smem) {
     constexpr int H = 4, RPS = 32 / H, WPB = kTB / 32;
@@ -559,6 +560,7 @@ struct SellPhaseA {
     h = wl % H;
     gw = int64_t(blockIdx.x) * WPB + warp;
     NW = int64_t(gridDim.x) * WPB;
+    pol = l2_keep_policy();
     // per warp K int2 {first entry row, local entry-row offset}, K x 32 lane
     // counts, TW x 32 column DoFs
     meta = reinterpret_cast<int2*>(smem) + warp * K;
@@ -587,14 +589,14 @@ struct SellPhaseA {
     for (int k = 0; k < kn; ++k) {
       const int2 m = meta[k];
       double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-      sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2);
+      sell_acc_cached<H>(SL, m.x, cols + m.y * 32, lhs[k * 32 + wl], wl, p, a0, a1, a2, pol);
       const int64_t q = (gw + k * NW) * RPS + grp;
       if (h == 0 && q < SL.nb - SL.r0) {
         const int64_t R = sell_row(SL, q);
         double* yo = hp + 3 * R;
-        yo[0] = a0;
-        yo[1] = a1;
-        yo[2] = a2;
+        st_keep(yo, a0, pol);
+        st_keep(yo + 1, a1, pol);
+        st_keep(yo + 2, a2, pol);
         dot += p[3 * R] * a0 + p[3 * R + 1] * a1 + p[3 * R + 2] * a2;
       }
     }
@@ -612,18 +614,18 @@ struct RowRegs {
 
 __device__ __forceinline__ void rowregs_load(RowRegs& q, int64_t b, const double* __restrict__ p,
                                              const double* __restrict__ r, const double* __restrict__ x,
-                                             const double* __restrict__ minv) {
-  load_vec3(p + 3 * b, q.p[0], q.p[1], q.p[2]);
-  load_vec3(r + 3 * b, q.r[0], q.r[1], q.r[2]);
-  load_vec3(x + 3 * b, q.x[0], q.x[1], q.x[2]);
+                                             const double* __restrict__ minv, uint64_t pol) {
+  load_vec3_keep(p + 3 * b, q.p[0], q.p[1], q.p[2], pol);
+  load_vec3_keep(r + 3 * b, q.r[0], q.r[1], q.r[2], pol);
+  load_vec3_keep(x + 3 * b, q.x[0], q.x[1], q.x[2], pol);
   load_block9(minv + 9 * b, q.M);
 }
 
 // x += a p, r -= a hp, z = M^-1 r (stores x, r; z stays in q), r.r / r.z partials
 __device__ __forceinline__ void rowregs_update(RowRegs& q, int64_t b, double alpha, const double* hp, double* x,
-                                               double* r, double (&v)[2]) {
+                                               double* r, double (&v)[2], uint64_t pol) {
   double hh[3];
-  load_vec3_cg(hp + 3 * b, hh[0], hh[1], hh[2]);
+  load_vec3_keep(hp + 3 * b, hh[0], hh[1], hh[2], pol);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     q.x[i] += alpha * q.p[i];
@@ -632,8 +634,8 @@ __device__ __forceinline__ void rowregs_update(RowRegs& q, int64_t b, double alp
   precond_apply<3>(q.M, q.r, q.z);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    x[3 * b + i] = q.x[i];
-    r[3 * b + i] = q.r[i];
+    st_keep(x + 3 * b + i, q.x[i], pol);
+    st_keep(r + 3 * b + i, q.r[i], pol);
     v[0] += q.r[i] * q.r[i];
     v[1] += q.r[i] * q.z[i];
   }
@@ -648,6 +650,7 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
   extern __shared__ double smem[];
   const int G = gridDim.x;
   A.prologue(smem);
+  const uint64_t kpol = l2_keep_policy();
   const int64_t nth = int64_t(G) * blockDim.x;
   const int64_t b0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool has0 = b0 < nb;
@@ -693,10 +696,10 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
     double v[2] = {0.0, 0.0};
     for (int64_t b = b0; b < nb; b += nth) {
       RowRegs q;
-      rowregs_load(q, b, p, r, x, minv);
-      rowregs_update(q, b, alpha, hp, x, r, v);
+      rowregs_load(q, b, p, r, x, minv, kpol);
+      rowregs_update(q, b, alpha, hp, x, r, v, kpol);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) z[3 * b + i] = q.z[i];
+      for (int i = 0; i < 3; ++i) st_keep(z + 3 * b + i, q.z[i], kpol);
     }
     block_reduce<2>(v);
     if (threadIdx.x == 0) {
@@ -733,10 +736,10 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
     // ---- phase C: p = z + beta p (this thread's own rows: z is its own write)
     for (int64_t b = b0; b < nb; b += nth) {
       double zz[3], pp[3];
-      load_vec3(z + 3 * b, zz[0], zz[1], zz[2]);
-      load_vec3(p + 3 * b, pp[0], pp[1], pp[2]);
+      load_vec3_keep(z + 3 * b, zz[0], zz[1], zz[2], kpol);
+      load_vec3_keep(p + 3 * b, pp[0], pp[1], pp[2], kpol);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) p[3 * b + i] = zz[i] + beta * pp[i];
+      for (int i = 0; i < 3; ++i) st_keep(p + 3 * b + i, zz[i] + beta * pp[i], kpol);
     }
     grid_arrive(cnt);
     grid_wait(cnt, (unsigned long long)G * ++epoch);
