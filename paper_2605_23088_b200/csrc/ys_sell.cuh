@@ -126,6 +126,20 @@ __device__ __forceinline__ void load_vec3_keep(const double* p, double& x0, doub
   }
 }
 
+__device__ __forceinline__ void load_block9_keep(const double* p, double (&v)[9], uint64_t pol) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const double2* w = reinterpret_cast<const double2*>(a & ~uintptr_t(15));
+  const double2 w0 = ld_keep2(w, pol), w1 = ld_keep2(w + 1, pol), w2 = ld_keep2(w + 2, pol),
+                w3 = ld_keep2(w + 3, pol), w4 = ld_keep2(w + 4, pol);
+  if (a & 8) {
+    v[0] = w0.y; v[1] = w1.x; v[2] = w1.y; v[3] = w2.x; v[4] = w2.y;
+    v[5] = w3.x; v[6] = w3.y; v[7] = w4.x; v[8] = w4.y;
+  } else {
+    v[0] = w0.x; v[1] = w0.y; v[2] = w1.x; v[3] = w1.y; v[4] = w2.x;
+    v[5] = w2.y; v[6] = w3.x; v[7] = w3.y; v[8] = w4.x;
+  }
+}
+
 // Same accumulation with the lane's column DoFs already in shared memory
 // (cols[j * 32 + lane], j < Lh) and its first entry row e0: the x gathers and
 // the value loads issue together.

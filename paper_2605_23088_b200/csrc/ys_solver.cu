@@ -618,7 +618,7 @@ __device__ __forceinline__ void rowregs_load(RowRegs& q, int64_t b, const double
   load_vec3_keep(p + 3 * b, q.p[0], q.p[1], q.p[2], pol);
   load_vec3_keep(r + 3 * b, q.r[0], q.r[1], q.r[2], pol);
   load_vec3_keep(x + 3 * b, q.x[0], q.x[1], q.x[2], pol);
-  load_block9(minv + 9 * b, q.M);
+  load_block9_keep(minv + 9 * b, q.M, pol);
 }
 
 // x += a p, r -= a hp, z = M^-1 r (stores x, r; z stays in q), r.r / r.z partials
