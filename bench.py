@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--state", default="rollout", choices=["rollout", "jitter"])
     p.add_argument("--frames", type=int, default=None, help="rollout frames (default: the config's, 25 for C5)")
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                   help="N>1: peer-memory persistent solve (default) or the NCCL-allgather loop")
     return p.parse_args()
 
 
@@ -333,7 +335,10 @@ def main():
     eng = sim.eng
     if world > 1:
         from paper_2605_23088_b200 import dist as ysdist
-        ysdist.init_nccl(eng)
+        if args.transport == "p2p":
+            ysdist.init_p2p(eng)
+        else:
+            ysdist.init_nccl(eng)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", local))
     cfg = sim.config
 
@@ -451,9 +456,12 @@ def main():
                    "prepared_frames": getattr(sim, "prepared_frames", 0),
                    "prepare_s": round(t_prep, 2),
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
-                   "parallelism": f"rows{world}: owned-row evaluation + row-partitioned PCG" if world > 1 else "single"},
+                   "parallelism": (f"rows{world}: owned-row evaluation + row-partitioned PCG ({args.transport})"
+                                   if world > 1 else "single")},
         "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else
-                     "row-partitioned PCG (k_dspmv_sell / k_dupdate per rank + NCCL allgather)",
+                     ("row-partitioned PCG: one persistent k_dpcg_p2p per rank, NVLink peer-memory exchanges"
+                      if args.transport == "p2p" else
+                      "row-partitioned PCG (k_dspmv_sell / k_dupdate per rank + NCCL allgather)"),
                      "bound": "hbm", "achieved": pcg_gbs, "peak": peak, "unit": "GB/s", "frac": pcg_gbs / peak,
                      "traffic": traffic_from_profiles(args.config, "pcg_dram_bytes_per_iteration"),
                      "algorithmic_bytes": pcg_iter_bytes,

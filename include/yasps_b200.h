@@ -283,15 +283,48 @@ int ys_dist_info(ys_context* ctx, int32_t* rank, int32_t* nranks, int64_t* bound
  * partition comes from the static structure) and the scene's total. */
 int ys_dist_eval_counts(ys_context* ctx, int64_t* evaluated, int64_t* total);
 
+/* Peer-memory transport (one NVSwitch node, <= 8 ranks): the same row
+ * partition, owned-row evaluation and recurrence, but ONE persistent
+ * cooperative kernel per rank runs the whole solve and exchanges through
+ * NVLink peer memory with device-side flags (no host round trip or
+ * collective launch per iteration): each rank stores the z of the rows its
+ * peers need straight into their windows (they form their halo p = z + beta p
+ * themselves), its partial sums into their value slots followed by a
+ * release-store of the exchange's sequence number, and at the end its rows of
+ * dx into every peer.  Partials are summed in rank order on every rank.
+ * Replaces the reference's sharded spmv_add (solver.cpp:59-82) across GPUs.
+ *
+ * open: allocate this rank's window (after ys_finalize) and return its
+ * cudaIpcMemHandle (64 bytes); connect: map every peer's window from the
+ * rank-major table of nranks handles (the caller all-gathers them, e.g. over
+ * torch.distributed).  ys_minimize_step then uses the peer-memory solve.
+ * probe: without `seen`, release-store rank+1 into every peer's probe slot;
+ * with `seen` (nranks values), read the slots the peers wrote (a mapping
+ * test that needs no spinning kernel). */
+int ys_dist_p2p_open(ys_context* ctx, int32_t rank, int32_t nranks, unsigned char handle[64]);
+int ys_dist_p2p_connect(ys_context* ctx, const unsigned char* handles);
+int ys_dist_p2p_probe(ys_context* ctx, int64_t* seen);
+/* n contexts of ONE process on ONE device as the n ranks of the peer-memory
+ * solve (the windows are plain device pointers), stepped together by
+ * ys_dist_p2p_group_step: every rank's pre-solve work (owned-row evaluation,
+ * assembly, preconditioner) in its own context, then one cooperative launch
+ * running all ranks' views of the solve kernel — the emulation of a
+ * multi-GPU job on one GPU (separate per-rank kernels that spin on each other
+ * cannot share a device).  dx: n step buffers or NULL; stats: n records. */
+int ys_dist_p2p_group(ys_context** ctxs, int32_t n);
+int ys_dist_p2p_group_step(ys_context** ctxs, int32_t n, double tol, int64_t max_iter, double** dx,
+                           ys_step_stats* stats);
+
 /* ------------------------------------------------------------------------
  * Benchmark hooks: per-stage device times of the last minimize_step, measured
  * with CUDA events on the context's stream (ms): [0] refresh_dynamic,
  * [1] local eval, [2] assembly gather, [3] preconditioner build, [4] PCG,
- * [5] SpMV (sum over iterations), [6] total; [8..11] persistent-PCG phase clocks,
+ * [5] SpMV (sum over iterations), [6] total, [7] the peer-memory solve kernel of the
+ * whole job (ys_dist_p2p_group_step); [8..11] persistent-PCG phase clocks,
  * [12..15] its sub-phase clocks (ms must hold 16 doubles).
  * counts[0] = kernel launches, counts[1] = indefinite 9x9 projections of the
  * last assembly, counts[2] = uniform-3x3 PCG path of the last solve (1 sliced-ELL
- * copy, 2 row gather from upper storage; 0 other), counts[3] = of the
+ * copy, 2 row gather from upper storage, 3 peer-memory distributed; 0 other), counts[3] = of the
  * indefinite projections, those done by the Jacobi fallback (counts must hold
  * 4 values).
  * ------------------------------------------------------------------------ */

@@ -148,12 +148,18 @@ _SIGS = {
     "dist_finalize": [_P],
     "dist_info": [_P, _PI32, _PI32, _PI64, _PI64, _PI64],
     "dist_eval_counts": [_P, _PI64, _PI64],
+    "dist_p2p_open": [_P, _I32, _I32, C.c_char_p],
+    "dist_p2p_connect": [_P, C.c_char_p],
+    "dist_p2p_probe": [_P, _PI64],
+    "dist_p2p_group": [C.POINTER(_P), _I32],
+    "dist_p2p_group_step": [C.POINTER(_P), _I32, _D, _I64, C.POINTER(_PD), C.POINTER(StepStats)],
 }
 _RESTYPES = {"destroy": None, "last_error": C.c_char_p, "version": C.c_char_p, "last_error_class": C.c_int}
 
 # Functions the oracle does not implement (device-only instrumentation).
 OPTIONAL = {"set_profiling", "stage_times", "device_bytes", "time_kernel", "stream", "set_option", "dist_unique_id",
-            "dist_init_nccl", "dist_eval_counts"}
+            "dist_init_nccl", "dist_eval_counts", "dist_p2p_open", "dist_p2p_connect", "dist_p2p_probe",
+            "dist_p2p_group", "dist_p2p_group_step"}
 
 
 class Library:

@@ -856,88 +856,99 @@ int ys_apply_hessian(ys_context* c, const double* x, double* y) {
   });
 }
 
+// Everything of a Newton iteration before the solve: dynamic rebuild, local
+// evaluation, assembly, block-Jacobi preconditioner (engine.cpp:75-95).
+static void step_prepare(Context* c) {
+  c->launches = 0;
+  c->sell_prepared = false;
+  if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  // The static energies' evaluation (SNH, inertia: nearly all of the local
+  // work) does not depend on the dynamic structure: it runs on a second
+  // stream while the dynamic group is rebuilt (whose host synchronisations
+  // would otherwise leave the device idle); ys_set_option("overlap", 0):
+  // sequential (bitwise the same step, tested).
+  if (c->dist.kind && c->dist.nranks > 1) ctx_dist_static_plan(*c);  // owned-row instance lists (once)
+  const bool overlap = c->overlap;
+  bool dyn_stencil = false;
+  for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
+  if (overlap && !dyn_stencil) {
+    if (!c->stream2) {
+      YS_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+      YS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      YS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    // the static energies on one side stream (pass B batched over all of
+    // them; two streams splitting even / odd energies measured slower once
+    // pass B was batched: C5 step 5.02 vs 4.97 ms)
+    c->evd_count.resize(std::max(c->evd_count.n, 2 * c->energies.size()));
+    c->evd_count.zero(c->stream);
+    YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+    YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+    ctx_eval_all(*c, true, true, 0, c->stream2, -1, false);
+    ctx_gather_all(*c, 0, c->stream2);
+    YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
+    try {
+      ctx_refresh_dynamic(*c, false);
+      // the solve's copy layout needs the structure only: built while the
+      // static evaluation still runs on the side stream
+      if (!c->dist.kind) pcg_prepare(*c);
+      ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
+    } catch (...) {
+      c->sell_prepared = false;
+      cudaStreamSynchronize(c->stream2);
+      throw;
+    }
+  } else {
+    ctx_refresh_dynamic(*c, false);
+    ctx_assemble(*c, true, true, -1, nullptr, false);
+  }
+  try {
+    ctx_build_preconditioner(*c);
+  } catch (...) {
+    c->sell_prepared = false;  // the prepared layout is consumed by this step's solve only
+    throw;
+  }
+  if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));
+}
+
+// After the solve: X0 <- X, the step to the host, stage clocks.
+static void step_finish(Context* c, double* dx) {
+  if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[6], c->stream));
+  YS_CUDA(cudaMemcpyAsync(c->X0.p, c->X.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (dx) c->DX.download(dx, size_t(c->s), c->stream);
+  YS_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->profiling) {
+    float ms = 0.f;
+    // [0] refresh [1] eval [2] gather [3] precond [4] pcg [6] total
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->stage_ms[0] = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+    c->stage_ms[1] = ms;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    c->stage_ms[2] = ms;
+    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
+    c->stage_ms[3] = ms;
+    cudaEventElapsedTime(&ms, c->ev[5], c->ev[6]);
+    c->stage_ms[4] = ms;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]);
+    c->stage_ms[6] = ms;
+  }
+}
+
 int ys_minimize_step(ys_context* c, double tol, int64_t max_iter, double* dx, ys_step_stats* stats) {
   return guarded(c, [&] {
     require_finalized(*c);
     auto t0 = std::chrono::steady_clock::now();
-    c->launches = 0;
-    c->sell_prepared = false;
-    if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
-    // The static energies' evaluation (SNH, inertia: nearly all of the local
-    // work) does not depend on the dynamic structure: it runs on a second
-    // stream while the dynamic group is rebuilt (whose host synchronisations
-    // would otherwise leave the device idle); ys_set_option("overlap", 0):
-    // sequential (bitwise the same step, tested).
-    if (c->dist.kind && c->dist.nranks > 1) ctx_dist_static_plan(*c);  // owned-row instance lists (once)
-    const bool overlap = c->overlap;
-    bool dyn_stencil = false;
-    for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
-    if (overlap && !dyn_stencil) {
-      if (!c->stream2) {
-        YS_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
-        YS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-        YS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-      }
-      // the static energies on one side stream (pass B batched over all of
-      // them; two streams splitting even / odd energies measured slower once
-      // pass B was batched: C5 step 5.02 vs 4.97 ms)
-      c->evd_count.resize(std::max(c->evd_count.n, 2 * c->energies.size()));
-      c->evd_count.zero(c->stream);
-      YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
-      YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
-      ctx_eval_all(*c, true, true, 0, c->stream2, -1, false);
-      ctx_gather_all(*c, 0, c->stream2);
-      YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
-      try {
-        ctx_refresh_dynamic(*c, false);
-        // the solve's copy layout needs the structure only: built while the
-        // static evaluation still runs on the side stream
-        if (!c->dist.kind) pcg_prepare(*c);
-        ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
-      } catch (...) {
-        c->sell_prepared = false;
-        cudaStreamSynchronize(c->stream2);
-        throw;
-      }
-    } else {
-      ctx_refresh_dynamic(*c, false);
-      ctx_assemble(*c, true, true, -1, nullptr, false);
-    }
+    step_prepare(c);
     const double t_asm = elapsed(t0);
-    try {
-      ctx_build_preconditioner(*c);
-    } catch (...) {
-      c->sell_prepared = false;  // the prepared layout is consumed by this step's solve only
-      throw;
-    }
-    if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));
     if (max_iter < 0) max_iter = std::max<int64_t>(2 * c->s, 64);
     ys_step_stats local{};
     if (c->dist.kind) ctx_dist_pcg(*c, tol, max_iter, &local);
     else ctx_pcg(*c, tol, max_iter, c->G.p, c->DX.p, &local);
-    if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[6], c->stream));
-    YS_CUDA(cudaMemcpyAsync(c->X0.p, c->X.p, c->s * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    if (dx) c->DX.download(dx, size_t(c->s), c->stream);
-    YS_CUDA(cudaStreamSynchronize(c->stream));
+    step_finish(c, dx);
     local.assemble_seconds = t_asm;
     local.solve_seconds = elapsed(t0) - t_asm;
     local.regularized_blocks = c->regularized;
-    if (c->profiling) {
-      float ms = 0.f;
-      // [0] refresh [1] eval [2] gather [3] precond [4] pcg [6] total
-      cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-      c->stage_ms[0] = ms;
-      cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
-      c->stage_ms[1] = ms;
-      cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
-      c->stage_ms[2] = ms;
-      cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
-      c->stage_ms[3] = ms;
-      cudaEventElapsedTime(&ms, c->ev[5], c->ev[6]);
-      c->stage_ms[4] = ms;
-      cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]);
-      c->stage_ms[6] = ms;
-    }
     if (stats) *stats = local;
   });
 }
@@ -1077,7 +1088,7 @@ int ys_set_profiling(ys_context* c, int32_t on) {
 
 int ys_stage_times(ys_context* c, double* ms, int64_t* counts) {
   return guarded(c, [&] {
-    for (int k = 0; k < 7; ++k) ms[k] = c->stage_ms[k];
+    for (int k = 0; k < 8; ++k) ms[k] = c->stage_ms[k];
     for (int k = 0; k < 8; ++k) ms[8 + k] = c->pcg_phase_ms[k];
     if (counts) {
       counts[0] = c->launches;
@@ -1289,6 +1300,68 @@ int ys_dist_eval_counts(ys_context* c, int64_t* evaluated, int64_t* total) {
       if (!e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING)) all += e.n;
     if (evaluated) *evaluated = part ? d.eval_owned : all;
     if (total) *total = all;
+  });
+}
+
+int ys_dist_p2p_open(ys_context* c, int32_t rank, int32_t nranks, unsigned char handle[64]) {
+  return guarded(c, [&] {
+    require_finalized(*c);
+    ctx_dist_p2p_open(*c, rank, nranks, handle);
+  });
+}
+
+int ys_dist_p2p_connect(ys_context* c, const unsigned char* handles) {
+  return guarded(c, [&] {
+    if (!handles) fail(YS_ERR_VALIDATION, "P2P solve: null handle table");
+    ctx_dist_p2p_connect(*c, handles);
+  });
+}
+
+int ys_dist_p2p_probe(ys_context* c, int64_t* seen) {
+  return guarded(c, [&] { ctx_dist_p2p_probe(*c, seen); });
+}
+
+static std::vector<Context*> group_of(ys_context** cs, int32_t n) {
+  if (!cs || n < 1 || n > kMaxP2P) fail(YS_ERR_VALIDATION, "P2P group: 1.." + std::to_string(kMaxP2P) + " contexts");
+  std::vector<Context*> v;
+  for (int k = 0; k < n; ++k) {
+    if (!cs[k]) fail(YS_ERR_VALIDATION, "P2P group: null context");
+    require_finalized(*cs[k]);
+    v.push_back(cs[k]);
+  }
+  return v;
+}
+
+int ys_dist_p2p_group(ys_context** cs, int32_t n) {
+  if (!cs || n < 1 || !cs[0]) return YS_ERR_VALIDATION;
+  return guarded(cs[0], [&] { ctx_dist_p2p_group(group_of(cs, n)); });
+}
+
+int ys_dist_p2p_group_step(ys_context** cs, int32_t n, double tol, int64_t max_iter, double** dx,
+                           ys_step_stats* stats) {
+  if (!cs || n < 1 || !cs[0]) return YS_ERR_VALIDATION;
+  return guarded(cs[0], [&] {
+    std::vector<Context*> g = group_of(cs, n);
+    for (int k = 0; k < n; ++k)
+      if (g[size_t(k)]->dist.kind != 3 || g[size_t(k)]->dist.p2p.group.size() != size_t(n) ||
+          g[size_t(k)]->dist.p2p.group[size_t(k)] != g[size_t(k)])
+        fail(YS_ERR_VALIDATION, "P2P group: the contexts were not grouped by ys_dist_p2p_group in this order");
+    auto t0 = std::chrono::steady_clock::now();
+    for (Context* c : g) {
+      YS_CUDA(cudaSetDevice(c->device));
+      step_prepare(c);
+    }
+    const double t_asm = elapsed(t0);
+    if (max_iter < 0) max_iter = std::max<int64_t>(2 * g[0]->s, 64);
+    std::vector<ys_step_stats> local(static_cast<size_t>(n));
+    ctx_dist_p2p_solve(g, tol, max_iter, local.data());
+    for (int k = 0; k < n; ++k) {
+      step_finish(g[size_t(k)], dx ? dx[k] : nullptr);
+      local[size_t(k)].assemble_seconds = t_asm;
+      local[size_t(k)].solve_seconds = elapsed(t0) - t_asm;
+      local[size_t(k)].regularized_blocks = g[size_t(k)]->regularized;
+      if (stats) stats[k] = local[size_t(k)];
+    }
   });
 }
 

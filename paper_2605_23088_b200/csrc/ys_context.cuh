@@ -163,8 +163,31 @@ struct PcgState {
 
 // Row-partitioned multi-GPU solve (ys_dist.cu).  The plan is rebuilt per
 // solve because the dynamic structure changes every Newton iteration.
+struct Context;
+constexpr int kMaxP2P = 8;  // ranks of the peer-memory solve (one NVSwitch node)
+
+// Peer-memory transport (kind 3, ys_dist.cu): one device allocation per rank
+// that the peers write into — exchange flags and values, the z rows the rank
+// receives as halo, and the step rows of every rank.
+struct P2PState {
+  char* win = nullptr;      // this rank's window (cudaMalloc; IPC-exported)
+  size_t win_bytes = 0;
+  int64_t win_s = 0;        // DoFs the window was sized for
+  void* peer[kMaxP2P] = {}; // peer windows (IPC-mapped, or the group's own windows)
+  bool ipc[kMaxP2P] = {};   // peer[k] came from cudaIpcOpenMemHandle
+  std::vector<Context*> group;  // emulated ranks of one process (all on one device), else empty
+  unsigned long long solve_id = 0;     // identical on every rank: flags are (solve_id << 32 | exchange)
+  DevBuf<uint32_t> mask;    // NB: ranks that need row R's z (bit k)
+  DevBuf<uint8_t> hflag;
+  DevBuf<int32_t> halo;     // rows owned elsewhere whose z this rank receives
+  DevBuf<int32_t> nhalo;
+  int64_t nhalo_host = 0;
+  DevBuf<unsigned long long> bar;  // rank-local grid barrier counter
+  int sm_share = 0;         // CTAs per rank of the last launch
+};
+
 struct DistState {
-  int kind = 0;  // 0 off, 1 host callback transport, 2 NCCL
+  int kind = 0;  // 0 off, 1 host callback transport, 2 NCCL, 3 peer memory (P2P)
   int rank = 0, nranks = 1;
   ys_allgather_fn fn = nullptr;
   void* user = nullptr;
@@ -189,6 +212,7 @@ struct DistState {
   int64_t eval_owned = 0, eval_total = 0;     // static stencil instances evaluated / in the scene
   std::vector<DevBuf<int32_t>> gsel;          // per static shape group: unique blocks touching owned rows
   std::vector<int64_t> ngsel;
+  P2PState p2p;
 };
 
 struct Context {
@@ -324,6 +348,11 @@ void ctx_dist_unique_id(unsigned char* id);
 void ctx_dist_init_nccl(Context& c, int rank, int nranks, const unsigned char* id);
 void ctx_dist_finalize(Context& c);
 void ctx_dist_static_plan(Context& c);  // partition + owned-row instance lists (once)
+void ctx_dist_p2p_open(Context& c, int rank, int nranks, unsigned char* handle);  // window + IPC handle
+void ctx_dist_p2p_connect(Context& c, const unsigned char* handles);            // map the peers' windows
+void ctx_dist_p2p_group(const std::vector<Context*>& cs);                       // emulated ranks, one device
+void ctx_dist_p2p_solve(const std::vector<Context*>& cs, double tol, int64_t max_iter, ys_step_stats* stats);
+void ctx_dist_p2p_probe(Context& c, int64_t* seen);
 uint64_t structure_checksum(Context& c, Structure& st, int64_t total_dofs);
 void ctx_refresh_pairs(Context& c, int pairset, double dhat, const int32_t* child_fixed,
                        int64_t* n_pairs);

@@ -52,3 +52,18 @@ def torch_allgather(group=None):
 def init_host(eng, group=None):
     import torch.distributed as dist
     eng.dist_init_host(dist.get_rank(group), dist.get_world_size(group), torch_allgather(group))
+
+
+def init_p2p(eng, group=None):
+    """Peer-memory transport (production multi-GPU path on one NVSwitch node):
+    every rank allocates its window, the 64-byte cudaIpcMemHandles are
+    all-gathered over the process group, every rank maps its peers' windows.
+    The solve then runs as one persistent kernel per rank exchanging through
+    NVLink stores and device-side flags."""
+    import torch.distributed as dist
+    rank, n = dist.get_rank(group), dist.get_world_size(group)
+    handle = eng.dist_p2p_open(rank, n)
+    handles = [None] * n
+    dist.all_gather_object(handles, handle, group=group)
+    eng.dist_p2p_connect(handles)
+    dist.barrier(group=group)  # every window mapped before any rank stores into it

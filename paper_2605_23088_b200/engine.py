@@ -416,6 +416,31 @@ class Engine:
         self._c(self.f["dist_finalize"](self.ctx))
         self._dist_cb = None
 
+    # peer-memory transport: one persistent kernel per rank, NVLink P2P stores
+    def dist_p2p_open(self, rank: int, nranks: int) -> bytes:
+        """Allocate this rank's window; returns its 64-byte cudaIpcMemHandle."""
+        if not self.lib.has("dist_p2p_open"):
+            raise _lib.DeclError(f"{self.lib.path.name} has no peer-memory transport")
+        buf = C.create_string_buffer(64)
+        self._c(self.f["dist_p2p_open"](self.ctx, int(rank), int(nranks), buf))
+        return buf.raw
+
+    def dist_p2p_connect(self, handles: list[bytes]):
+        """Map every peer's window (handles: one 64-byte handle per rank, rank order)."""
+        table = b"".join(bytes(h) for h in handles)
+        if any(len(h) != 64 for h in handles):
+            raise _lib.ValidationError("cudaIpcMemHandle must be 64 bytes")
+        self._c(self.f["dist_p2p_connect"](self.ctx, table))
+
+    def dist_p2p_probe(self, read: bool) -> np.ndarray | None:
+        """read=False: store rank+1 into every peer's probe slot; read=True: the slots peers wrote."""
+        if not read:
+            self._c(self.f["dist_p2p_probe"](self.ctx, None))
+            return None
+        seen = np.zeros(64, dtype=np.int64)
+        self._c(self.f["dist_p2p_probe"](self.ctx, seen.ctypes.data_as(_lib._PI64)))
+        return seen[:self.dist_info()["nranks"]]
+
     def dist_info(self) -> dict:
         rank, nranks = C.c_int32(), C.c_int32()
         bounds = np.zeros(65, dtype=np.int64)
@@ -629,3 +654,25 @@ class BlockSystem:
         self.eng._c(self.eng.f["bsr_pcg"](self.eng.ctx, self.id, int(block_size), _dp(gv), float(tol),
                                           int(max_iter), _dp(x), C.byref(it), C.byref(rel), C.byref(conv)))
         return x, it.value, rel.value, bool(conv.value)
+
+
+def p2p_group(engines: list["Engine"]):
+    """Make the engines (one process, one device, the same scene) the ranks of
+    the peer-memory solve; step them with p2p_group_step (the one-GPU
+    emulation of a multi-GPU job: one cooperative launch runs every rank)."""
+    n = len(engines)
+    arr = (C.c_void_p * n)(*[e.ctx for e in engines])
+    check(engines[0].lib, engines[0].ctx, engines[0].f["dist_p2p_group"](arr, n))
+
+
+def p2p_group_step(engines: list["Engine"], tol: float, max_iter: int = -1, want_dx: bool = True) -> list[Step]:
+    n = len(engines)
+    arr = (C.c_void_p * n)(*[e.ctx for e in engines])
+    dxs = [np.zeros(e.s) for e in engines] if want_dx else None
+    dxp = (_lib._PD * n)(*[_dp(d) for d in dxs]) if want_dx else None
+    stats = (StepStats * n)()
+    check(engines[0].lib, engines[0].ctx,
+          engines[0].f["dist_p2p_group_step"](arr, n, float(tol), int(max_iter), dxp, stats))
+    return [Step(dxs[k] if want_dx else None, stats[k].pcg_iterations, stats[k].pcg_residual,
+                 bool(stats[k].pcg_converged), stats[k].regularized_blocks, stats[k].assemble_seconds,
+                 stats[k].solve_seconds) for k in range(n)]

@@ -43,9 +43,10 @@ def test_b200_library_exports_every_declared_symbol():
 def test_oracle_exports_the_same_abi():
     lib = oracle.library()
     dll = lib.dll
-    # device instrumentation and the NCCL transport have no CPU counterpart
+    # device instrumentation and the NCCL / peer-memory transports have no CPU counterpart
     optional = {"ys_set_profiling", "ys_stage_times", "ys_device_bytes", "ys_time_kernel", "ys_dist_unique_id",
-                "ys_dist_init_nccl"}
+                "ys_dist_init_nccl", "ys_dist_p2p_open", "ys_dist_p2p_connect", "ys_dist_p2p_probe",
+                "ys_dist_p2p_group", "ys_dist_p2p_group_step"}
     missing = [n for n in declared() if n not in optional and not hasattr(dll, "yo_" + n[3:])]
     assert not missing, missing
 
