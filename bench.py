@@ -382,7 +382,12 @@ def main():
     eng.set_profiling(False)
 
     peak, peak_src = load_peaks()
-    spmv_ms, spmv_bytes = eng.time_kernel(3, 50)  # the PCG's SpMV: sliced-ELL copy, 4 lanes per row
+    try:
+        spmv_ms, spmv_bytes = eng.time_kernel(3, 50)  # the PCG's SpMV: sliced-ELL copy, 4 lanes per row
+        spmv_kind = "k_spmv_sell<4> (sliced-ELL full copy of static + dynamic H), timed alone"
+    except _lib.ValidationError:  # mixed block sizes (C3: affine bodies): the row-gather SpMV
+        spmv_ms, spmv_bytes = eng.time_kernel(0, 50)
+        spmv_kind = "k_spmv_gen (row gather from upper storage, per block-size class), timed alone"
     asm_ms, asm_bytes = eng.time_kernel(1, 10)
     eval_ms, _ = eng.time_kernel(2, 5)
     fp64_ms, fp64_flops = eng.time_kernel(4, 5)  # FP64 FMA peak probe (this box, this run)
@@ -397,6 +402,7 @@ def main():
     nb = eng.s // 3
     pcg_iter_bytes = spmv_bytes + 72.0 * nb + 16.0 * eng.s + 48.0 * eng.s
     pcg_ms = stages[4]
+    pcg_path = eng.pcg_path()
     pcg_gbs = pcg_iter_bytes * st.pcg_iterations / (pcg_ms * 1e-3) / 1e9
 
     # e2e through the C-ABI with pinned host buffers: positions + pair table in, dx out
@@ -458,7 +464,10 @@ def main():
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
                    "parallelism": (f"rows{world}: owned-row evaluation + row-partitioned PCG ({args.transport})"
                                    if world > 1 else "single")},
-        "roofline": {"kernel": "k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)" if world == 1 else
+        "roofline": {"kernel": ("k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)"
+                                if pcg_path == "sliced-ELL copy" else
+                                "k_pcg_gen_persistent (whole PCG solve, warp per block row of each block-size class, one cooperative launch)")
+                     if world == 1 else
                      ("row-partitioned PCG: one persistent k_dpcg_p2p per rank, NVLink peer-memory exchanges"
                       if args.transport == "p2p" else
                       "row-partitioned PCG (k_dspmv_sell / k_dupdate per rank + NCCL allgather)"),
@@ -467,7 +476,7 @@ def main():
                      "algorithmic_bytes": pcg_iter_bytes,
                      "algorithmic_bytes_unit": "per PCG iteration", "iterations": int(st.pcg_iterations),
                      "avg_launch_ms": pcg_ms, "peak_source": peak_src,
-                     "spmv": {"kernel": "k_spmv_sell<4> (sliced-ELL full copy of static + dynamic H), timed alone",
+                     "spmv": {"kernel": spmv_kind,
                               "achieved": spmv_gbs, "frac": spmv_gbs / peak, "algorithmic_bytes": spmv_bytes,
                               "traffic": traffic_from_profiles(args.config, "spmv_dram_bytes"),
                               "avg_launch_ms": spmv_ms}},

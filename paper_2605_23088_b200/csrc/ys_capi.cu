@@ -313,7 +313,12 @@ int ys_create(ys_context** out, int32_t device) {
   if (prop.major != 10) return YS_ERR_CUDA;  // built for sm_100a only; no fallback
   auto* c = new ys_context();
   c->device = device;
-  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  // the context stream at the highest priority: while the static evaluation
+  // fills the device from the low-priority side stream, the dynamic rebuild's
+  // short kernels are dispatched first as SMs free up
+  int prio_lo = 0, prio_hi = 0;
+  if (cudaSetDevice(device) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     delete c;
     return YS_ERR_CUDA;
   }
@@ -873,7 +878,9 @@ static void step_prepare(Context* c) {
   for (auto& e : c->energies) dyn_stencil |= e.dynamic && (e.kind == K_SNH || e.kind == K_BENDING);
   if (overlap && !dyn_stencil) {
     if (!c->stream2) {
-      YS_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+      int lo = 0, hi = 0;
+      YS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      YS_CUDA(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, c->eval_low_priority ? lo : hi));
       YS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
       YS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
@@ -1370,6 +1377,7 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
     const std::string n = name ? name : "";
     if (n == "overlap") c->overlap = value != 0;
     else if (n == "pcg_copy") c->pcg_copy = value != 0;
+    else if (n == "eval_low_priority") c->eval_low_priority = value != 0;  // before the first overlapped step
     else if (n == "eval_evd") {
       if (value < 0 || value > 2)
         fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi), 1 (clamped eigenpairs) or 2 (every element through the fallback)");

@@ -304,6 +304,7 @@ struct Context {
   // profiling
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
+  bool eval_low_priority = true;  // side stream of the static evaluation below the context stream's priority
   bool pcg_copy = true;  // uniform 3x3 solve over the sliced-ELL copy (false: the row-gather kernel; tests)
   int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only,
                        // 2 every element handed to the fallback list (tests)

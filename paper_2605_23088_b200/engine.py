@@ -572,7 +572,7 @@ class Engine:
         ms = np.zeros(16)
         cnt = np.zeros(4, dtype=np.int64)
         self._c(self.f["stage_times"](self.ctx, _dp(ms), _ip64(cnt)))
-        return {1: "sliced-ELL copy", 2: "row gather"}.get(int(cnt[2]), "general")
+        return {1: "sliced-ELL copy", 2: "row gather", 3: "peer-memory distributed"}.get(int(cnt[2]), "general")
 
     def time_kernel(self, which: int, reps: int = 20):
         ms, b = C.c_double(), C.c_double()
