@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "ys_contact4.cuh"
 #include "ys_device.cuh"
 
@@ -709,6 +711,38 @@ __global__ void k_gather_h(const int64_t* __restrict__ seg, const uint32_t* __re
   values[voff[u] + e] = acc;
 }
 
+// The same with the blocks taken in a given order (k-th slot -> order[k]):
+// the static group's blocks sorted by run length, so the lanes of a warp sum
+// runs of similar length (in the structure's own (row, col) order every few
+// blocks a ~24-long vertex run sits next to ~5-long edge runs and the warp
+// waits for the longest).  Each block's sum keeps its left-to-right order:
+// bit-identical values.  RC is a compile-time constant (no 64-bit division).
+template <int RC>
+__global__ void k_gather_h_ord(const int64_t* __restrict__ seg, const uint32_t* __restrict__ perm,
+                               const double* __restrict__ hc, const int32_t* __restrict__ order, int nsel,
+                               const int64_t* __restrict__ voff, double* __restrict__ values) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nsel * RC) return;
+  const int k = t / RC, e = t - k * RC;
+  const int64_t u = order[k];
+  const int64_t j0 = seg[u], j1 = seg[u + 1];
+  double acc = 0.0;
+  for (int64_t j = j0; j < j1; ++j) acc += hc[perm[j] + e];
+  values[voff[u] + e] = acc;
+}
+
+__global__ void k_run_keys(const int64_t* __restrict__ seg, int64_t u0, int64_t n, int wshift,
+                           uint32_t* __restrict__ key, int32_t* __restrict__ val) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  // sorted inside windows of 2^wshift consecutive blocks: similar lengths per warp,
+  // while the window keeps the element contributions its blocks share close
+  // (a global sort by length scattered them: 0.31 -> 0.41 ms at C5)
+  const int64_t len = seg[u0 + k + 1] - seg[u0 + k];
+  key[k] = (uint32_t(k >> wshift) << 10) | uint32_t(len < 1023 ? len : 1023);
+  val[k] = int32_t(u0 + k);
+}
+
 // The same over a selection of unique blocks (the distributed solve's owned
 // rows).
 __global__ void k_gather_h_sel(const int64_t* __restrict__ seg, const uint32_t* __restrict__ perm,
@@ -849,11 +883,12 @@ __device__ __forceinline__ int jacobi_block_inverse(const double* B, double* inv
   return 2;
 }
 
-template <int N>
+template <int N, bool WITH_G = true>
 __device__ __forceinline__ void block_row_work(int64_t b, const BlocksDev& B, const GroupView& S0,
                                                const GroupView& S1, double* G, double* diag, double* minv,
                                                int32_t* bflag, int want_h) {
   const int32_t st = B.start[b];
+  if (WITH_G) {
   double acc[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) acc[k] = 0.0;
@@ -870,6 +905,7 @@ __device__ __forceinline__ void block_row_work(int64_t b, const BlocksDev& B, co
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) G[st + k] = acc[k];
+  }
   if (!want_h) return;
   double blk[N * N];
 #pragma unroll
@@ -908,6 +944,34 @@ __global__ void k_block_rows(BlocksDev B, const int32_t* __restrict__ list, int6
   if (q >= nb) return;
   const int64_t b = list ? list[q] : b0 + q;
   block_row_work<N>(b, B, S0, S1, G, diag, minv, bflag, want_h);
+}
+
+// Uniform small blocks: the gradient gather with one thread per DoF (the
+// row's N sums in parallel, each in block_row_work's order: bit-identical),
+// then k_block_rows<N, false> for the diagonal block and its inverse.
+template <int N>
+__global__ void k_grad_rows(BlocksDev B, int64_t nb, GroupView S0, GroupView S1, double* G, int64_t b0) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nb * N) return;
+  const int64_t b = b0 + t / N;
+  const int k = int(t % N);
+  double acc = 0.0;
+#pragma unroll
+  for (int gi = 0; gi < 2; ++gi) {
+    const GroupView& S = gi == 0 ? S0 : S1;
+    if (!S.gseg) continue;
+    const int32_t j0 = S.gseg[b], j1 = S.gseg[b + 1];
+    for (int32_t j = j0; j < j1; ++j) acc += S.gcontrib[(S.gperm[j] & 0x0FFFFFFFu) + k];
+  }
+  G[B.start[b] + k] = acc;
+}
+
+template <int N>
+__global__ void k_block_rows_h(BlocksDev B, int64_t nb, GroupView S0, GroupView S1, double* diag, double* minv,
+                               int32_t* bflag, int64_t b0) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nb) return;
+  block_row_work<N, false>(b0 + q, B, S0, S1, nullptr, diag, minv, bflag, 1);
 }
 
 // Large blocks (affine bodies' 9x9 A block, 12x12): a warp per block row.
@@ -1200,6 +1264,33 @@ void ctx_eval_all(Context& c, bool project, bool with_hessian, int only, cudaStr
   }
 }
 
+// Run-length order of the static structure's blocks (once per structure; own
+// temporaries: this runs on the side stream next to the dynamic rebuild).
+static void build_gather_order(Structure& st, int wshift, cudaStream_t s) {
+  st.gorder.clear();
+  st.gorder.resize(st.groups.size());
+  for (size_t gi = 0; gi < st.groups.size(); ++gi) {
+    const auto& g = st.groups[gi];
+    const int64_t cnt = g[3];
+    if (cnt == 0) continue;
+    DevBuf<uint32_t> kin, kout;
+    DevBuf<int32_t> vin;
+    DevBuf<char> tmp;
+    kin.resize(size_t(cnt));
+    kout.resize(size_t(cnt));
+    vin.resize(size_t(cnt));
+    st.gorder[gi].resize(size_t(cnt));
+    k_run_keys<<<grid_for(cnt), kTB, 0, s>>>(st.seg.p, g[2], cnt, wshift, kin.p, vin.p);
+    YS_LAUNCH_CHECK();
+    size_t bytes = 0;
+    YS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.p, kout.p, vin.p, st.gorder[gi].p, int(cnt), 0, 32, s));
+    tmp.resize(std::max<size_t>(bytes, 1));
+    YS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, kin.p, kout.p, vin.p, st.gorder[gi].p, int(cnt), 0, 32, s));
+    YS_CUDA(cudaStreamSynchronize(s));
+  }
+  st.gorder_valid = true;
+}
+
 void ctx_gather_all(Context& c, int only, cudaStream_t s) {
   if (!s) s = c.stream;
   for (int w = 0; w < 2; ++w) {
@@ -1221,8 +1312,14 @@ void ctx_gather_all(Context& c, int only, cudaStream_t s) {
         ++c.launches;
         continue;
       }
-      k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc, st.voff.p,
-                                                    st.values.p);
+      if (w == 0 && rc == 9 && cnt * 9 < (int64_t(1) << 31)) {
+        if (!st.gorder_valid) build_gather_order(st, c.gather_wshift, s);
+        k_gather_h_ord<9><<<grid_for(cnt * 9), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, st.gorder[gi].p,
+                                                           int(cnt), st.voff.p, st.values.p);
+      } else {
+        k_gather_h<<<grid_for(cnt * rc), kTB, 0, s>>>(st.seg.p, st.perm.p, st.hcontrib.p, g[2], cnt, rc, st.voff.p,
+                                                      st.values.p);
+      }
       YS_LAUNCH_CHECK();
       ++c.launches;
     }
@@ -1275,6 +1372,17 @@ void ctx_block_rows(Context& c, bool want_h) {
         k_block_rows_warp<12><<<gw, 128, 0, c.stream>>>(B, list, nb, S0, S1, c.G.p, c.diag.p, c.minv.p, c.bflag.p, wh);
       YS_LAUNCH_CHECK();
       ++c.launches;
+      continue;
+    }
+    if (c.rc_classes[k] == 3 && !list) {
+      k_grad_rows<3><<<grid_for(nb * 3, 128), 128, 0, c.stream>>>(B, nb, S0, S1, c.G.p, b0);
+      YS_LAUNCH_CHECK();
+      ++c.launches;
+      if (want_h) {
+        k_block_rows_h<3><<<g, 128, 0, c.stream>>>(B, nb, S0, S1, c.diag.p, c.minv.p, c.bflag.p, b0);
+        YS_LAUNCH_CHECK();
+        ++c.launches;
+      }
       continue;
     }
 #define YS_ROWS(N)                                                                                            \

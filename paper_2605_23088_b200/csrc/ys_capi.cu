@@ -1378,6 +1378,11 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
     if (n == "overlap") c->overlap = value != 0;
     else if (n == "pcg_copy") c->pcg_copy = value != 0;
     else if (n == "eval_low_priority") c->eval_low_priority = value != 0;  // before the first overlapped step
+    else if (n == "gather_window") {
+      if (value < 0 || value > 20) fail(YS_ERR_VALIDATION, "gather_window must be 0..20 (log2 of the window)");
+      c->gather_wshift = int(value);
+      c->S[0].gorder_valid = false;
+    }
     else if (n == "eval_evd") {
       if (value < 0 || value > 2)
         fail(YS_ERR_VALIDATION, "eval_evd must be 0 (Jacobi), 1 (clamped eigenpairs) or 2 (every element through the fallback)");

@@ -129,6 +129,10 @@ struct Structure {
   DevBuf<int64_t> seg;          // n_blocks + 1
   DevBuf<uint32_t> perm;        // double offset of each sorted contribution
   DevBuf<double> hcontrib;
+  // static gather order: per shape group, its unique blocks sorted by run
+  // length (a warp's lanes then sum runs of similar length)
+  std::vector<DevBuf<int32_t>> gorder;
+  bool gorder_valid = false;
   // gradient plan: slot contributions sorted by gstart; segment per block row.
   int64_t n_gcontrib = 0;
   DevBuf<int32_t> gseg;         // NB + 1
@@ -304,7 +308,8 @@ struct Context {
   // profiling
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
-  bool eval_low_priority = true;  // side stream of the static evaluation below the context stream's priority
+  bool eval_low_priority = true;
+  int gather_wshift = 12;  // static gather order: run-length sort inside windows of 2^wshift blocks  // side stream of the static evaluation below the context stream's priority
   bool pcg_copy = true;  // uniform 3x3 solve over the sliced-ELL copy (false: the row-gather kernel; tests)
   int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only,
                        // 2 every element handed to the fallback list (tests)

@@ -328,6 +328,7 @@ void build_structure_from_keys(Context& c, Structure& st, DevBuf<uint64_t>& keys
   cudaStream_t s = c.stream;
   st.n_contrib = n;
   st.checksum_valid = false;
+  st.gorder_valid = false;
   st.diag_uid.resize(size_t(blocks.nb));
   if (blocks.nb) k_fill_i32<<<grid_for(blocks.nb), kTB, 0, s>>>(st.diag_uid.p, blocks.nb, -1);
   if (n == 0) {
