@@ -790,16 +790,21 @@ __device__ __forceinline__ void lu_inverse(const double* B, double* inv) {
         best = fabs(a[r * N + k]);
         p = r;
       }
-    if (p != k) {
+    // swap rows k and p by static selects (a runtime row index would move a
+    // and piv to local memory)
 #pragma unroll
-      for (int c = 0; c < N; ++c) {
-        const double t = a[k * N + c];
-        a[k * N + c] = a[p * N + c];
-        a[p * N + c] = t;
+    for (int r = k + 1; r < N; ++r) {
+      if (r == p) {
+#pragma unroll
+        for (int c = 0; c < N; ++c) {
+          const double t = a[k * N + c];
+          a[k * N + c] = a[r * N + c];
+          a[r * N + c] = t;
+        }
+        const int t = piv[k];
+        piv[k] = piv[r];
+        piv[r] = t;
       }
-      const int t = piv[k];
-      piv[k] = piv[p];
-      piv[p] = t;
     }
     const double d = a[k * N + k];
 #pragma unroll
