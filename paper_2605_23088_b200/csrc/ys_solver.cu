@@ -19,6 +19,7 @@
 //    p update) captured into a CUDA graph with a conditional WHILE node that
 //    loops on the device until the status word leaves 0.
 #include <algorithm>
+#include <cstdio>
 #include <string>
 #include <cstdlib>
 #include <chrono>
@@ -1081,7 +1082,16 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         }
       }
       if (!launched) {
-        // row gather from upper storage (no copy, no shared-memory plan)
+        // row gather from upper storage (no copy, no shared-memory plan):
+        // ~0.36 of HBM against the copy's ~0.54 — said once per context, and
+        // reported by ys_stage_times (counts[2] = 2)
+        if (c.pcg_copy && !c.warned_pcg_fallback) {
+          std::fprintf(stderr,
+                       "yasps_b200: the sliced-ELL PCG plan (%lld slices) does not fit in shared memory; "
+                       "solving over the slower row gather from upper storage\n",
+                       (long long)c.sell_slices);
+          c.warned_pcg_fallback = true;
+        }
         void* kern = reinterpret_cast<void*>(k_pcg33_persistent<kTB, kSpmvMinB, 0>);
         int occ = 0;
         YS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTB, 0));
