@@ -1378,6 +1378,10 @@ int ys_set_option(ys_context* c, const char* name, int64_t value) {
     if (n == "overlap") c->overlap = value != 0;
     else if (n == "pcg_copy") c->pcg_copy = value != 0;
     else if (n == "eval_low_priority") c->eval_low_priority = value != 0;  // before the first overlapped step
+    else if (n == "pcg_ctas") {
+      if (value < 0 || value > 3) fail(YS_ERR_VALIDATION, "pcg_ctas must be 0 (auto) .. 3 (CTAs per SM)");
+      c->pcg_ctas = int(value);
+    }
     else if (n == "gather_window") {
       if (value < 0 || value > 20) fail(YS_ERR_VALIDATION, "gather_window must be 0..20 (log2 of the window)");
       c->gather_wshift = int(value);

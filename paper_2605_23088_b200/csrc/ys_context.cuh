@@ -309,7 +309,8 @@ struct Context {
   bool profiling = false;
   bool overlap = true;  // static evaluation on side streams during the dynamic rebuild (ys_set_option)
   bool eval_low_priority = true;
-  bool warned_pcg_fallback = false;  // the row-gather PCG fallback was announced
+  bool warned_pcg_fallback = false;
+  int pcg_ctas = 0;  // CTAs per SM of the persistent uniform-3x3 PCG (0: the most that fit)  // the row-gather PCG fallback was announced
   int gather_wshift = 12;  // static gather order: run-length sort inside windows of 2^wshift blocks  // side stream of the static evaluation below the context stream's priority
   bool pcg_copy = true;  // uniform 3x3 solve over the sliced-ELL copy (false: the row-gather kernel; tests)
   int evd_mode = 1;     // pass-B projection: 1 clamped-eigenpair path + Jacobi fallback, 0 Jacobi only,

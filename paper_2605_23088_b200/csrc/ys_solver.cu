@@ -1055,7 +1055,7 @@ void ctx_pcg(Context& c, double tol, int64_t max_iter, const double* g_dev, doub
         SellDev sl = sell_dev(c);
         void* kern = (void*)k_pcg33_stream<SellPhaseA>;
         const int wpb = kTB / 32;
-        for (int per = kSpmvMinB; per >= 1 && !launched; --per) {
+        for (int per = c.pcg_ctas > 0 ? std::min(c.pcg_ctas, kSpmvMinB) : kSpmvMinB; per >= 1 && !launched; --per) {
           // small systems: no more CTAs than give every warp two slices (at
           // least one per SM) — the grid barriers get cheaper with fewer CTAs
           int gsz = int(std::min<int64_t>(int64_t(per) * sm_count(),
