@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -230,6 +231,21 @@ class Engine {
   }
   int64_t total_dofs() const { return s_; }
   ys_context* raw() { return ctx_; }
+
+  // ---- several GPUs of one node: peer-memory row-partitioned solve.  open()
+  // returns this rank's 64-byte window handle; the caller all-gathers the
+  // handles (MPI, torch.distributed, ...) in rank order and connects.
+  std::array<unsigned char, 64> p2p_open(int32_t rank, int32_t nranks) {
+    std::array<unsigned char, 64> h{};
+    check(ys_dist_p2p_open(ctx_, rank, nranks, h.data()));
+    return h;
+  }
+  void p2p_connect(const std::vector<std::array<unsigned char, 64>>& handles) {
+    std::vector<unsigned char> table;
+    for (const auto& h : handles) table.insert(table.end(), h.begin(), h.end());
+    check(ys_dist_p2p_connect(ctx_, table.data()));
+  }
+  void dist_finalize() { check(ys_dist_finalize(ctx_)); }
 
  private:
   void check(int status) const {
