@@ -142,3 +142,42 @@ def test_p2p_ipc_mapping_two_processes():
     for r in range(2):
         assert isinstance(res[r], list), res[r]
         assert res[r] == [0 if j == r else j + 1 for j in range(2)]
+
+
+def _single_rank_worker(port, out):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        from paper_2605_23088_b200 import dist as ysdist
+        ref = _sim()
+        st_ref = ref.eng.minimize_step(1e-4)
+        sim = _sim()
+        ysdist.init_p2p(sim.eng)  # the multi-process path: window, handle all-gather, connect
+        steps = [sim.eng.minimize_step(1e-4) for _ in range(2)]
+        out.put(("ok", st_ref.pcg_iterations, st_ref.dx, [(s.pcg_iterations, s.dx) for s in steps],
+                 sim.eng.pcg_path()))
+    except Exception as e:  # surface worker failures to the test
+        out.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_process_path_single_rank():
+    """ys_minimize_step through the per-process launch (one view per kernel, as
+    on an 8-GPU box), here with one rank: same step as the single-GPU solve."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_single_rank_worker, args=(29750 + os.getpid() % 200, q))
+    p.start()
+    r = q.get(timeout=600)
+    p.join(timeout=60)
+    assert r[0] == "ok", r
+    _, it_ref, dx_ref, steps, path = r
+    assert path == "peer-memory distributed"
+    for it, dx in steps:
+        assert it == it_ref
+        assert np.max(np.abs(dx - dx_ref)) <= 1e-10 * np.max(np.abs(dx_ref))
