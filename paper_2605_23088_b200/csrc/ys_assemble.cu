@@ -727,7 +727,19 @@ __global__ void k_gather_h_ord(const int64_t* __restrict__ seg, const uint32_t* 
   const int64_t u = order[k];
   const int64_t j0 = seg[u], j1 = seg[u + 1];
   double acc = 0.0;
-  for (int64_t j = j0; j < j1; ++j) acc += hc[perm[j] + e];
+  // chunks of 8: the offsets, then the values, all in flight together; the
+  // sum stays left to right
+  for (int64_t j = j0; j < j1; j += 8) {
+    uint32_t off[8];
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) off[q] = j + q < j1 ? perm[j + q] : 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = j + q < j1 ? hc[off[q] + e] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j + q < j1) acc += v[q];
+  }
   values[voff[u] + e] = acc;
 }
 
