@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
   long long it = 0;
   double rel = st->rel, php = 0.0, alpha = 0.0;
   unsigned long long ph[4] = {0, 0, 0, 0};
+  unsigned long long aux[2] = {0, 0};
   unsigned long long epoch = 0;
   unsigned long long* cnt = &gb->arrivals;
   unsigned long long t0 = gtimer();
@@ -600,12 +601,14 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
 #pragma unroll
       for (int i = 0; i < 3; ++i) st_keep(z + 3 * b + i, q.z[i], kpol);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) aux[0] += gtimer() - t0;  // sub-phase: rows done (CTA 0 thread 0)
     block_reduce<2>(v);
     if (threadIdx.x == 0) {
       part[G + blockIdx.x] = v[0];
       part[2 * G + blockIdx.x] = v[1];
     }
     grid_arrive(cnt);
+    if (blockIdx.x == 0 && threadIdx.x == 0) aux[1] += gtimer() - t0;  // arrived
     grid_wait(cnt, (unsigned long long)G * ++epoch);
     t1 = gtimer();
     ph[1] += t1 - t0;
@@ -655,6 +658,8 @@ __global__ void __launch_bounds__(kTB, kSpmvMinB) k_pcg33_stream(PA A, int64_t n
     st->status = status;
     if (status == 3 || status == 4) st->fail_it = int(it - (status == 4 ? 1 : 0));
     for (int k = 0; k < 4; ++k) st->phase_ns[k] = ph[k];
+    st->aux_ns[0] = aux[0];
+    st->aux_ns[1] = aux[1];
   }
 }
 
