@@ -25,20 +25,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-def _sim(name="c1", jitter=0.0025):
+def _sim(name="c1", jitter=0.0025, **kw):
     from paper_2605_23088_b200 import configs
     from paper_2605_23088_b200.scene import SimConfig
     from backends import simulation
-    sim = simulation(SimConfig.from_dict(configs.CONFIGS[name]()), "gpu")
+    sim = simulation(SimConfig.from_dict(configs.CONFIGS[name](**kw)), "gpu")
     configs.jitter_targets(sim, jitter)
     sim.begin_frame()
     sim.refresh_dynamic_pairs()
     return sim
 
 
-def _group(n, name="c1", jitter=0.0025):
+def _group(n, name="c1", jitter=0.0025, **kw):
     from paper_2605_23088_b200.engine import p2p_group
-    sims = [_sim(name, jitter) for _ in range(n)]
+    sims = [_sim(name, jitter, **kw) for _ in range(n)]
     p2p_group([s.eng for s in sims])
     return sims
 
@@ -96,6 +96,23 @@ def test_p2p_group_c2_contact():
         assert np.array_equal(st.dx, steps[0].dx)
         assert residual(st.dx) <= max(10 * r_ref, 1e-9)
         assert np.max(np.abs(st.dx - st_ref.dx)) <= 1e-5 * np.max(np.abs(st_ref.dx))
+
+
+def test_p2p_group_cloth_bending():
+    """A C4-shaped cloth (bending hinges + inertia + cloth-sphere contact) on 2
+    ranks: owned-row bending evaluation and the peer-memory solve."""
+    from paper_2605_23088_b200.engine import p2p_group_step
+    ref = _sim("c4", 0.002, nx=24)
+    st_ref = ref.eng.minimize_step(1e-6)
+    sims = _group(2, "c4", 0.002, nx=24)
+    steps = p2p_group_step([s.eng for s in sims], 1e-6)
+    for st in steps:
+        assert st.pcg_converged == st_ref.pcg_converged
+        assert abs(st.pcg_iterations - st_ref.pcg_iterations) <= max(2, 0.02 * st_ref.pcg_iterations)
+        assert np.array_equal(st.dx, steps[0].dx)
+        assert np.max(np.abs(st.dx - st_ref.dx)) <= 1e-6 * np.max(np.abs(st_ref.dx))
+    ev = [s.eng.dist_info()["eval_instances"] for s in sims]
+    assert all(e < sims[0].eng.dist_info()["eval_total"] for e in ev)
 
 
 def test_p2p_group_bounds_match_host_transport():
