@@ -335,9 +335,9 @@ def main():
     eng = sim.eng
     if world > 1:
         from paper_2605_23088_b200 import dist as ysdist
-        if args.transport == "p2p":
-            ysdist.init_p2p(eng)
-        else:
+        if args.transport == "p2p" and not ysdist.init_p2p(eng):
+            args.transport = "nccl (peer memory unavailable on this node)"  # said on stderr by init_p2p
+        if not args.transport.startswith("p2p"):
             ysdist.init_nccl(eng)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=torch.device("cuda", local))
     cfg = sim.config

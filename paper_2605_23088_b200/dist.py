@@ -54,16 +54,30 @@ def init_host(eng, group=None):
     eng.dist_init_host(dist.get_rank(group), dist.get_world_size(group), torch_allgather(group))
 
 
-def init_p2p(eng, group=None):
+def init_p2p(eng, group=None) -> bool:
     """Peer-memory transport (production multi-GPU path on one NVSwitch node):
     every rank allocates its window, the 64-byte cudaIpcMemHandles are
     all-gathered over the process group, every rank maps its peers' windows.
     The solve then runs as one persistent kernel per rank exchanging through
-    NVLink stores and device-side flags."""
+    NVLink stores and device-side flags.  Returns True on every rank when every
+    rank mapped every peer; otherwise every rank returns False with its windows
+    released (collective decision: no rank is left waiting on another)."""
     import torch.distributed as dist
     rank, n = dist.get_rank(group), dist.get_world_size(group)
     handle = eng.dist_p2p_open(rank, n)
     handles = [None] * n
     dist.all_gather_object(handles, handle, group=group)
-    eng.dist_p2p_connect(handles)
-    dist.barrier(group=group)  # every window mapped before any rank stores into it
+    why = ""
+    try:
+        eng.dist_p2p_connect(handles)
+    except Exception as e:  # noqa: BLE001 - decided collectively below
+        why = repr(e)
+    oks = [None] * n
+    dist.all_gather_object(oks, why, group=group)  # also the barrier: every window mapped before any store
+    bad = [w for w in oks if w]
+    if bad:
+        eng.dist_finalize()
+        import sys
+        print(f"yasps_b200: peer-memory transport unavailable ({bad[0]})", file=sys.stderr)
+        return False
+    return True

@@ -134,7 +134,7 @@ def _ipc_worker(rank, world, port, out):
     try:
         from paper_2605_23088_b200 import dist as ysdist
         sim = _sim()
-        ysdist.init_p2p(sim.eng)
+        assert ysdist.init_p2p(sim.eng)
         sim.eng.dist_p2p_probe(False)  # rank+1 into every peer's window (NVLink / IPC store)
         dist.barrier()
         seen = sim.eng.dist_p2p_probe(True)
@@ -172,7 +172,7 @@ def _single_rank_worker(port, out):
         ref = _sim()
         st_ref = ref.eng.minimize_step(1e-4)
         sim = _sim()
-        ysdist.init_p2p(sim.eng)  # the multi-process path: window, handle all-gather, connect
+        assert ysdist.init_p2p(sim.eng)  # the multi-process path: window, handle all-gather, connect
         steps = [sim.eng.minimize_step(1e-4) for _ in range(2)]
         out.put(("ok", st_ref.pcg_iterations, st_ref.dx, [(s.pcg_iterations, s.dx) for s in steps],
                  sim.eng.pcg_path()))
