@@ -487,6 +487,16 @@ __global__ void k_flag_owned_blocks(const int32_t* __restrict__ row, const int32
   flag[t] = ((R >= r0 && R < r1) || (C >= r0 && C < r1)) ? 1 : 0;
 }
 
+// Sort key of selected block k: (window of 4096 positions, run length).
+__global__ void k_sel_run_keys(const int64_t* __restrict__ seg, const int32_t* __restrict__ sel, int64_t n,
+                               uint32_t* __restrict__ key) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t u = sel[k];
+  const int64_t len = seg[u + 1] - seg[u];
+  key[k] = (uint32_t(k >> 12) << 10) | uint32_t(len < 1023 ? len : 1023);
+}
+
 // Instance i of a 4-vertex stencil energy touches rows [r0, r1) (uniform 3x3).
 __global__ void k_flag_owned(const int4* __restrict__ conn, int64_t n, int32_t startP, int64_t r0, int64_t r1,
                              uint8_t* __restrict__ flag) {
@@ -570,6 +580,23 @@ void ctx_dist_static_plan(Context& c) {
     YS_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     YS_CUDA(cudaStreamSynchronize(s));
     d.ngsel[gi] = h;
+    // the gather order of the single-GPU static gather: run length sorted inside
+    // windows of 4096 selected blocks (bit-identical sums, warps of similar runs)
+    if (h > 1) {
+      DevBuf<uint32_t> kin, kout;
+      DevBuf<int32_t> vout;
+      kin.resize(size_t(h));
+      kout.resize(size_t(h));
+      vout.resize(size_t(h) + 1);
+      k_sel_run_keys<<<blocks_for(h), kTB, 0, s>>>(st0.seg.p, d.gsel[gi].p, h, kin.p);
+      YS_LAUNCH_CHECK();
+      size_t bytes = 0;
+      YS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.p, kout.p, d.gsel[gi].p, vout.p, h, 0, 32, s));
+      c.cubtmp.resize(std::max(c.cubtmp.n, bytes + 1));
+      YS_CUDA(cub::DeviceRadixSort::SortPairs(c.cubtmp.p, bytes, kin.p, kout.p, d.gsel[gi].p, vout.p, h, 0, 32, s));
+      YS_CUDA(cudaStreamSynchronize(s));
+      std::swap(d.gsel[gi], vout);
+    }
   }
   // instances outside the subset are never evaluated while the partition is
   // active: their contributions read as zero (non-owned rows are neither
