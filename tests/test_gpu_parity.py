@@ -373,3 +373,33 @@ def test_row_gather_pcg_path(name):
     assert pg == "row gather"
     assert sg.pcg_iterations == so.pcg_iterations
     assert np.max(np.abs(sg.dx - so.dx)) <= 1e-9 * np.max(np.abs(so.dx))
+
+
+@pytest.mark.parametrize("opt,values,bitwise", [
+    ("gather_window", [12, 4, 20], True),       # static gather order: every block's sum keeps its order
+    ("eval_low_priority", [1, 0], True),        # side-stream priority: scheduling only
+    ("pcg_ctas", [0, 2, 1], False),             # CTA count: the partial sums' grouping changes the rounding
+])
+def test_execution_options_keep_the_step(opt, values, bitwise):
+    """Execution options never change results beyond rounding: the static
+    gather order and the stream priority are bitwise neutral; the PCG's CTA
+    count regroups the dot-product partials (same iteration count, dx within
+    1e-10 at C2)."""
+    from paper_2605_23088_b200 import configs
+    from paper_2605_23088_b200.scene import SimConfig, Simulation
+
+    outs = []
+    for v in values:
+        sim = Simulation(SimConfig.from_dict(configs.c2()))
+        sim.eng.set_option(opt, v)
+        configs.jitter_targets(sim, 0.001)
+        sim.begin_frame()
+        sim.refresh_dynamic_pairs()
+        st = sim.eng.minimize_step(1e-4)
+        outs.append((st.dx, st.pcg_iterations))
+    for dx, it in outs[1:]:
+        assert it == outs[0][1]
+        if bitwise:
+            assert np.array_equal(dx, outs[0][0])
+        else:
+            assert np.max(np.abs(dx - outs[0][0])) <= 1e-10 * np.max(np.abs(outs[0][0]))
