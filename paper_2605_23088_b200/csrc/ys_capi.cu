@@ -866,6 +866,7 @@ int ys_apply_hessian(ys_context* c, const double* x, double* y) {
 static void step_prepare(Context* c) {
   c->launches = 0;
   c->sell_prepared = false;
+  c->sell_filled = false;
   if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[0], c->stream));
   // The static energies' evaluation (SNH, inertia: nearly all of the local
   // work) does not depend on the dynamic structure: it runs on a second
@@ -900,8 +901,17 @@ static void step_prepare(Context* c) {
       // static evaluation still runs on the side stream
       if (!c->dist.kind) pcg_prepare(*c);
       ctx_assemble(*c, true, true, 1, c->ev_join, false);  // errors checked by ctx_build_preconditioner
+      // the copy's values (assembled H only) on the side stream, beside the
+      // gradient / preconditioner pass on the context stream
+      if (!c->dist.kind && c->sell_prepared) {
+        YS_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+        YS_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+        sell_fill_early(*c, c->stream2);
+        YS_CUDA(cudaEventRecord(c->ev_join, c->stream2));
+      }
     } catch (...) {
       c->sell_prepared = false;
+      c->sell_filled = false;
       cudaStreamSynchronize(c->stream2);
       throw;
     }
@@ -911,8 +921,11 @@ static void step_prepare(Context* c) {
   }
   try {
     ctx_build_preconditioner(*c);
+    if (c->sell_filled) YS_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   } catch (...) {
     c->sell_prepared = false;  // the prepared layout is consumed by this step's solve only
+    c->sell_filled = false;
+    if (c->stream2) cudaStreamSynchronize(c->stream2);
     throw;
   }
   if (c->profiling) YS_CUDA(cudaEventRecord(c->ev[5], c->stream));

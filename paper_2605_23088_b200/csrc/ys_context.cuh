@@ -280,6 +280,7 @@ struct Context {
   int sell_tw_host = 0;
   int sell_h = 0;
   bool sell_prepared = false;  // layout built by sell_prepare, values not yet filled
+  bool sell_filled = false;    // values filled by sell_fill_early (the step's solve consumes them)
   int64_t sell_rows = 0, sell_slices = 0;  // entry rows, slices
   int64_t sell_r0 = 0, sell_r1 = 0;         // block-row range of the copy
 
@@ -379,6 +380,7 @@ BlocksDev blocks_view(Context& c);
 void drop_pcg_graph(Context& c);
 void sell_build(Context& c, int lanes_per_row, int64_t r0 = 0, int64_t r1 = -1);  // ys_sell.cu
 void sell_prepare(Context& c, int lanes_per_row, int64_t r0 = 0, int64_t r1 = -1);  // ys_sell.cu
+void sell_fill_early(Context& c, cudaStream_t s);                                    // ys_sell.cu
 void pcg_prepare(Context& c);  // ys_solver.cu
 void spmv_sell(Context& c, const double* x, double* y);
 int sell_max_warp_rows(Context& c, int64_t warps, int slices_per_warp);   // y = H x through the sliced-ELL copy

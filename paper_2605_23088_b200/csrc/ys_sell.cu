@@ -220,8 +220,27 @@ void sell_prepare(Context& c, int H, int64_t r0, int64_t r1) {
   c.sell_prepared = true;
 }
 
+// The values of the prepared single-GPU copy, filled on stream s (the side
+// stream, beside the preconditioner build): the next sell_build(c, 4) finds
+// them ready.
+void sell_fill_early(Context& c, cudaStream_t s) {
+  if (!(c.sell_prepared && c.sell_h == 4 && c.sell_r0 == 0 && c.sell_r1 == c.NB) || c.NB == 0) return;
+  c.sell_prepared = false;
+  const bool has1 = c.S[1].n_blocks > 0;
+  SpmvDev d0 = spmv_dev(c.S[0]);
+  SpmvDev d1 = has1 ? spmv_dev(c.S[1]) : d0;
+  k_sell_fill_lanes<<<int(ceil_div(c.sell_slices * 32, kTB)), kTB, 0, s>>>(
+      d0, d1, has1 ? 1 : 0, 0, c.NB, 4, c.sell_perm.p, SellOut{c.sell_soff.p, c.sell_col.p, c.sell_val.p, 4, 0});
+  YS_LAUNCH_CHECK();
+  c.sell_filled = true;
+}
+
 void sell_build(Context& c, int H, int64_t r0, int64_t r1) {
   if (r1 < 0) r1 = c.NB;
+  if (c.sell_filled) {
+    c.sell_filled = false;
+    if (c.sell_h == H && c.sell_r0 == r0 && c.sell_r1 == r1) return;  // filled by sell_fill_early
+  }
   const bool ready = c.sell_prepared && c.sell_h == H && c.sell_r0 == r0 && c.sell_r1 == r1;
   c.sell_prepared = false;
   if (!ready) sell_layout(c, H, r0, r1);
