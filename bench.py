@@ -464,7 +464,7 @@ def main():
                    "l2": "inputs larger than L2 (device working set %.2f GB >> 126 MB)" % (eng.device_bytes() / 1e9),
                    "parallelism": (f"rows{world}: owned-row evaluation + row-partitioned PCG ({args.transport})"
                                    if world > 1 else "single")},
-        "roofline": {"kernel": ("k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; the repack is included in avg_launch_ms)"
+        "roofline": {"kernel": ("k_pcg33_stream<SellPhaseA> (whole PCG solve over the sliced-ELL copy, one cooperative launch; avg_launch_ms = the solve stage: k_pcg_init + the persistent kernel; the copy's value fill runs before it, beside the preconditioner build)"
                                 if pcg_path == "sliced-ELL copy" else
                                 "k_pcg_gen_persistent (whole PCG solve, warp per block row of each block-size class, one cooperative launch)")
                      if world == 1 else
